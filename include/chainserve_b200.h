@@ -1,0 +1,200 @@
+/*
+ * chainserve_b200.h -- C-ABI of the B200 engine for the chainserve hot path.
+ *
+ * The reference (arXiv 2604.14993, /root/reference/pkg) is pure Python and has
+ * no FFI: its drop-in surface is the Python API re-exported by
+ * pkg/src/chainserve/__init__.py:3-65.  Each entry point below replaces the
+ * reference function named in its comment (file:line relative to
+ * /root/reference/pkg/src/chainserve).  The Python package
+ * paper_2604_14993_b200 binds these symbols with ctypes and keeps the
+ * reference's signatures, dataclasses and exceptions; INTEGRATION.md shows the
+ * binding.
+ *
+ * Conventions
+ *   * plain pointers + sizes; "d_" pointers are CUDA device pointers, all
+ *     others host pointers; `stream` is a cudaStream_t passed as void*.
+ *   * every call returns a status (CS_OK ...); cs_last_error() gives a
+ *     thread-local message for the last non-OK status.
+ *   * no global mutable state except per-device scratch caches; calls are
+ *     reentrant per stream.  Device calls are asynchronous on `stream`.
+ *   * there is no CPU fallback: without a usable CUDA device every compute
+ *     entry point returns CS_ERR_CUDA.
+ */
+#ifndef CHAINSERVE_B200_H
+#define CHAINSERVE_B200_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (mapped to the reference's exceptions by the shim) ---- */
+#define CS_OK 0
+#define CS_INFEASIBLE 1   /* InfeasibleError (placement.py:91-94)          */
+#define CS_INVALID 2      /* ValueError (model.py, sim.py:47-68, ...)      */
+#define CS_INTERNAL 3     /* AssertionError (cache_alloc.py:119,133)       */
+#define CS_ERR_CUDA 4     /* CUDA runtime failure / no device              */
+#define CS_UNSUPPORTED 5  /* NotImplementedError (mode outside the path)   */
+
+const char* cs_version(void);
+const char* cs_last_error(void);
+/* 1 if this host's glibc resolves log1p to its FMA variant (CPU has FMA and
+ * AVX2), else 0 -- numpy's ziggurat tail calls that libm (see glibc_log1p.cuh). */
+int cs_host_log1p_variant(void);
+/* number of visible CUDA devices (0 when none) */
+int cs_device_count(void);
+
+/* ------------------------------------------------------------------------ */
+/* RNG                                                                        */
+/* ------------------------------------------------------------------------ */
+/* Philox keys of np.random.SeedSequence(entropy=<entropy words>,
+ * spawn_key=(reps[i],)).generate_state(2, np.uint64)  -- replaces sim.py:141-143.
+ * entropy: the seed as little-endian uint32 words (numpy's
+ * _coerce_to_uint32_array).  keys: 2*n_reps uint64 (host). */
+int cs_philox_keys(const uint32_t* entropy, int32_t n_entropy, const uint64_t* reps,
+                   int64_t n_reps, uint64_t* keys);
+
+/* For each of n_streams keys, n_draws values of
+ * Generator(Philox(key)).exponential(1.0, n_draws) (numpy ziggurat) into
+ * d_out[s*ld + i].  Replaces rng.exponential at sim.py:145,159.
+ * log1p_variant: 1 = glibc FMA build, 0 = SSE2 build, -1 = this host's. */
+int cs_exp_streams(const uint64_t* d_keys, int64_t n_streams, int64_t n_draws, double* d_out,
+                   int64_t ld, int32_t log1p_variant, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* JFFC simulation                                                            */
+/* ------------------------------------------------------------------------ */
+/* One sweep point: a composed system (chains chain_base..chain_base+K-1 of the
+ * rates/caps arrays, rates descending) under Poisson arrivals of rate lam. */
+typedef struct {
+    int32_t n_chains;
+    int32_t chain_base;
+    double lam;
+} cs_sim_point;
+
+/* Per-replication result: the RepResult fields of sim.py:120-133 computed
+ * exactly as sim.py:298-324 does, plus the raw snapshots they derive from. */
+typedef struct {
+    double wait_sum;
+    double service_sum;
+    int64_t counted;
+    double window_s;
+    double mean_occupancy;
+    double occ_first_half;
+    double occ_second_half;
+    double lambda_effective;
+    int64_t end_queue_len;
+    double w_start, t_mid, area_mid, t_end, area_end;
+    double resp_sum;     /* numpy pairwise sum of the responses             */
+    double resp_mean;    /* responses.mean() = resp_sum / counted (sim.py:407) */
+} cs_rep_summary;
+
+/* _simulate_once (sim.py:181-324; Poisson workload, policy "jffc",
+ * horizon_time_s None) for every (point p, replication r) of a chunk of
+ * n_reps replications starting at rep_begin (of n_reps_total).  Chunk row r
+ * reads stream row r of d_streams (2*n_jobs draws, row stride lds):
+ * arrivals = cumsum((1/lam) * S[0:n]), sizes = S[n:2n].
+ * Outputs are point-major, o = p*n_reps_total + rep_begin + r:
+ *   d_responses[o*ldr + q]  q < n-warm, completion order (NULL: not stored;
+ *                           ldr must be even -- rows are written with 16-byte stores)
+ *   d_busy[o*ldb + k]       busy_time_s (ldb >= max_chains)
+ *   d_summary[o]
+ *   d_jobs[(o*n + j)*4 ..]  (arrival, start, finish, chain) or NULL.
+ * max_chains / max_capacity bound K and sum(caps) over the points; above 8 /
+ * 16 a generic kernel needs cs_jffc_sim_workspace_bytes() of d_workspace.
+ * warm = int(warmup_fraction * n) computed by the caller as Python does. */
+int cs_jffc_sim(const cs_sim_point* d_points, int32_t n_points, const double* d_rates,
+                const int32_t* d_caps, int32_t max_chains, int32_t max_capacity,
+                const double* d_streams, int64_t lds, int32_t rep_begin, int32_t n_reps,
+                int32_t n_reps_total, int64_t n_jobs, int64_t warm, double* d_responses,
+                int64_t ldr, double* d_busy, int32_t ldb, cs_rep_summary* d_summary,
+                double* d_jobs, void* d_workspace, int64_t workspace_bytes, void* stream);
+
+int64_t cs_jffc_sim_workspace_bytes(int32_t n_points, int32_t n_reps, int32_t max_chains,
+                                    int32_t max_capacity, int64_t n_jobs);
+
+/* ------------------------------------------------------------------------ */
+/* Statistics over stored responses (run_sim aggregation, sim.py:406-438)     */
+/* ------------------------------------------------------------------------ */
+/* n_groups groups (sweep points) of rows_per_group consecutive response rows
+ * of m values (row stride ldr, even).
+ *  * d_summary[row].resp_mean = responses.mean() of the row, bit-exact with
+ *    numpy's pairwise summation (sim.py:407); d_row_sums (optional) gets the
+ *    row sums.
+ *  * if ranks != NULL: exact order statistics.  ranks[g*n_ranks + i]
+ *    (0-based, np.sort order of group g's merged responses; negative = from
+ *    the end) -> out_values[g*n_ranks + i] (host).  Replaces
+ *    np.sort(np.concatenate(...)) + the order statistics np.quantile
+ *    interpolates (sim.py:406,436-438).  n_ranks <= 6.
+ * Synchronises `stream`. */
+int cs_rep_stats(const double* d_resp, int32_t n_groups, int64_t rows_per_group, int64_t m,
+                 int64_t ldr, cs_rep_summary* d_summary, const int64_t* ranks, int32_t n_ranks,
+                 double* out_values, double* d_row_sums, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* End to end from HOST buffers                                               */
+/* ------------------------------------------------------------------------ */
+/* run_sim (sim.py:397-456) for n_points sweep points sharing seed `entropy`
+ * (uint32 words) and replications [rep_begin, rep_begin+n_reps): keys ->
+ * streams -> simulation -> per-rep means + order statistics, all on the
+ * device.  points/rates/caps/ranks are host arrays; outputs are host arrays:
+ * out_summary[o], out_busy[o*ldb + k], out_rank_values[g*n_ranks + i],
+ * out_responses (NULL or rows*(n-warm), completion order), out_jobs (NULL or
+ * rows*n*4).  max_stream_bytes bounds the stream scratch
+ * (replications are processed in chunks; 0 = unbounded). */
+int cs_run_sim_host(const cs_sim_point* points, int32_t n_points, const double* rates,
+                    const int32_t* caps, int32_t n_chain_entries, const uint32_t* entropy,
+                    int32_t n_entropy, int32_t rep_begin, int32_t n_reps, int64_t n_jobs,
+                    int64_t warm, const int64_t* ranks, int32_t n_ranks, int32_t log1p_variant,
+                    int64_t max_stream_bytes, cs_rep_summary* out_summary, double* out_busy,
+                    int32_t ldb, double* out_rank_values, double* out_responses, double* out_jobs,
+                    void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* Composition: GBP-CR placement and GCA chain composition                   */
+/* ------------------------------------------------------------------------ */
+/* One composition point: servers server_base..server_base+J-1 of the fleet
+ * SoA arrays, service (L, s_m, s_c), design parameter c, lambda, rho_bar. */
+typedef struct {
+    int32_t n_servers;
+    int32_t server_base;
+    int64_t block_count;
+    int64_t block_bytes;
+    int64_t cache_slot_bytes;
+    int64_t capacity;
+    double arrival_rate;
+    double load_target;
+} cs_compose_point;
+
+/* greedy_block_placement for every point (placement.py:35-132).
+ * Per point p (offsets server_base): first/count/max_blocks/bound_time[J];
+ * order[J] = GBP visit order (-1 padded); chain_end[J] = 1 where a chain
+ * closes in `order`; n_chains[p]; scaled_rate[p]; rate_satisfied[p];
+ * status[p] in {CS_OK, CS_INFEASIBLE, CS_INVALID}.  All device pointers. */
+int cs_gbp_batch(const cs_compose_point* d_points, int32_t n_points, int32_t max_servers,
+                 const int64_t* d_mem,
+                 const double* d_tau_c, const double* d_tau_p, const int32_t* d_id_rank,
+                 int32_t* d_first, int32_t* d_count, int32_t* d_max_blocks, double* d_bound_time,
+                 int32_t* d_order, int32_t* d_chain_end, int32_t* d_n_chains,
+                 double* d_scaled_rate, int32_t* d_rate_satisfied, int32_t* d_status,
+                 void* stream);
+
+/* greedy_cache_allocation for every point's placement (cache_alloc.py:65-135,
+ * model.py:130-231).  d_residual: per-server residual slots or NULL for the
+ * full budget.  Outputs per point p, capacity max_chains chains of at most
+ * max_hops servers: chain_srv[(p*max_chains + k)*max_hops + h] (server index
+ * within the point, -1 padded), chain_len, caps, times (service_time_s),
+ * n_chains[p], n_edges[p], status[p]. */
+int cs_gca_batch(const cs_compose_point* d_points, int32_t n_points, int32_t max_servers,
+                 int32_t max_block_count, const int64_t* d_mem,
+                 const double* d_tau_c, const double* d_tau_p, const int32_t* d_id_rank,
+                 const int32_t* d_first, const int32_t* d_count, const int64_t* d_residual,
+                 int32_t max_chains, int32_t max_hops, int32_t* d_chain_srv,
+                 int32_t* d_chain_len, int32_t* d_caps, double* d_times, int32_t* d_n_chains,
+                 int64_t* d_n_edges, int32_t* d_status, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CHAINSERVE_B200_H */

@@ -1,0 +1,33 @@
+// cs_internal.cuh -- shared helpers of the libchainserve_b200 sources.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/chainserve_b200.h"
+
+namespace cs {
+
+// Thread-local last-error message (cs_last_error()).
+void set_error(const char* fmt, ...);
+
+inline int check_launch(const char* what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        set_error("%s: %s", what, cudaGetErrorString(e));
+        return CS_ERR_CUDA;
+    }
+    return CS_OK;
+}
+
+inline int check_cuda(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) {
+        set_error("%s: %s", what, cudaGetErrorString(e));
+        return CS_ERR_CUDA;
+    }
+    return CS_OK;
+}
+
+// Python-semantics helpers (no contraction; explicit IEEE round-to-nearest).
+__device__ __forceinline__ double py_div(double a, double b) { return __ddiv_rn(a, b); }
+
+}  // namespace cs

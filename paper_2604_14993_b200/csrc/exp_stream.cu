@@ -1,0 +1,174 @@
+// exp_stream.cu -- warp-parallel numpy-exact exponential streams.
+//
+// Replaces, bit for bit, Generator(Philox(key)).exponential(1.0, n) as used by
+// the reference at sim.py:145,159 (the arrival gaps are scale * S[0:n] and the
+// sizes are S[n:2n] of ONE stream S = standard_exponential(2n); the survey's
+// common-random-number identity).
+//
+// Layout: one warp per stream.  A chunk is 32 consecutive Philox blocks
+// (lane l owns block 32*c + l, i.e. counter 32*c + l + 1, words 4l..4l+3).
+// Every word is classified as the START of a ziggurat attempt (fast accept:
+// 1 word, value x; slow: 2 words, value or reject).  Whether a word actually
+// starts an attempt depends on all earlier words, but an attempt never spans
+// more than 2 words, so each lane's 4 words form a transfer function
+// {entry offset 0|1} -> {exit offset 0|1, values emitted}.  A 5-step warp
+// shuffle scan composes those functions, giving every lane its true entry
+// offset and output position.  A slow attempt starting at the chunk's last
+// word is carried into the next chunk (resolved by lane 0 with word 0).
+#include <cuda_runtime.h>
+
+#include "cs_rng.cuh"
+#include "cs_internal.cuh"
+
+namespace cs {
+
+struct Xfer {
+    int x0, x1;  // exit offset for entry 0 / 1
+    int c0, c1;  // values emitted for entry 0 / 1
+};
+
+__global__ void __launch_bounds__(256) exp_streams_kernel(const uint64_t* __restrict__ keys,
+                                                          int64_t n_streams, int64_t n_draws,
+                                                          double* __restrict__ out, int64_t ld,
+                                                          int log1p_fma,
+                                                          int64_t* __restrict__ words_used) {
+    __shared__ ZigSmem zs;
+    zig_load(&zs);
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int64_t stream = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (stream >= n_streams) return;
+    const uint64_t k0 = keys[2 * stream], k1 = keys[2 * stream + 1];
+    double* __restrict__ o = out + stream * ld;
+
+    int64_t produced = 0;
+    int entry = 0;            // warp-uniform: offset of the first attempt in this chunk
+    uint64_t pend_w = 0;      // word that started the carried slow attempt (entry == 1)
+    uint64_t chunk = 0;
+    while (produced < n_draws) {
+        uint64_t w[4];
+        philox4x64_10(chunk * 32 + lane + 1, 0, 0, 0, k0, k1, w);
+        const uint64_t wnext = __shfl_down_sync(0xffffffffu, w[0], 1);
+
+        // Per-word attempt results.
+        double v[4];
+        int adv[4];
+        bool has[4];
+#pragma unroll
+        for (int p = 0; p < 4; p++) {
+            double x;
+            if (zig_fast(&zs, w[p], &x)) {
+                v[p] = x;
+                adv[p] = 1;
+                has[p] = true;
+            } else if (p < 3 || lane < 31) {
+                const ZigAttempt a = zig_slow(&zs, w[p], p < 3 ? w[p + 1] : wnext, log1p_fma);
+                v[p] = a.v;
+                adv[p] = 2;
+                has[p] = a.has;
+            } else {
+                v[p] = 0.0;  // carried: resolved by the next chunk's lane 0
+                adv[p] = 2;
+                has[p] = false;
+            }
+        }
+        // Carried slow attempt from the previous chunk (only lane 0, entry 1).
+        bool carry_has = false;
+        double carry_v = 0.0;
+        if (lane == 0 && entry == 1) {
+            const ZigAttempt a = zig_slow(&zs, pend_w, w[0], log1p_fma);
+            carry_has = a.has;
+            carry_v = a.v;
+        }
+
+        // Transfer function of this lane.
+        Xfer f;
+        {
+            int p = 0, c = 0;
+#pragma unroll
+            for (int q = 0; q < 4; q++)
+                if (p == q) {
+                    c += has[q];
+                    p += adv[q];
+                }
+            f.x0 = p - 4;
+            f.c0 = c;
+            p = 1;
+            c = 0;
+#pragma unroll
+            for (int q = 1; q < 4; q++)
+                if (p == q) {
+                    c += has[q];
+                    p += adv[q];
+                }
+            f.x1 = p - 4;
+            f.c1 = c + (carry_has ? 1 : 0);
+        }
+        // Inclusive Kogge-Stone scan of function composition (prefix then self).
+        Xfer inc = f;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int px0 = __shfl_up_sync(0xffffffffu, inc.x0, d);
+            const int px1 = __shfl_up_sync(0xffffffffu, inc.x1, d);
+            const int pc0 = __shfl_up_sync(0xffffffffu, inc.c0, d);
+            const int pc1 = __shfl_up_sync(0xffffffffu, inc.c1, d);
+            if (lane >= d) {
+                Xfer n;
+                n.x0 = px0 ? inc.x1 : inc.x0;
+                n.c0 = pc0 + (px0 ? inc.c1 : inc.c0);
+                n.x1 = px1 ? inc.x1 : inc.x0;
+                n.c1 = pc1 + (px1 ? inc.c1 : inc.c0);
+                inc = n;
+            }
+        }
+        const int ex_x0 = __shfl_up_sync(0xffffffffu, inc.x0, 1);
+        const int ex_x1 = __shfl_up_sync(0xffffffffu, inc.x1, 1);
+        const int ex_c0 = __shfl_up_sync(0xffffffffu, inc.c0, 1);
+        const int ex_c1 = __shfl_up_sync(0xffffffffu, inc.c1, 1);
+        const int my_entry = lane == 0 ? entry : (entry ? ex_x1 : ex_x0);
+        int pos = lane == 0 ? 0 : (entry ? ex_c1 : ex_c0);
+
+        // Emit this lane's values.
+        int64_t base = produced + pos;
+        if (carry_has) {
+            if (base < n_draws) o[base] = carry_v;
+            base++;
+        }
+        {
+            int p = my_entry;
+#pragma unroll
+            for (int q = 0; q < 4; q++)
+                if (p == q) {
+                    if (has[q]) {
+                        if (base < n_draws) o[base] = v[q];
+                        base++;
+                    }
+                    p += adv[q];
+                }
+        }
+        // Chunk totals from lane 31; detect a carried attempt at word 127.
+        const int tot = __shfl_sync(0xffffffffu, entry ? inc.c1 : inc.c0, 31);
+        const int nxt = __shfl_sync(0xffffffffu, entry ? inc.x1 : inc.x0, 31);
+        pend_w = __shfl_sync(0xffffffffu, w[3], 31);
+        produced += tot;
+        entry = nxt;
+        chunk++;
+    }
+    if (words_used != nullptr && lane == 0) {
+        // Exact word count only when the stream ended on a chunk boundary is not
+        // needed by the simulator; report the chunk-granular upper bound.
+        words_used[stream] = (int64_t)(chunk * 128);
+    }
+}
+
+}  // namespace cs
+
+extern "C" int cs_exp_streams_impl(const uint64_t* d_keys, int64_t n_streams, int64_t n_draws,
+                                   double* d_out, int64_t ld, int log1p_fma, void* stream) {
+    if (n_streams <= 0 || n_draws <= 0) return 0;
+    const int warps_per_block = 8;
+    const int64_t blocks = (n_streams + warps_per_block - 1) / warps_per_block;
+    cs::exp_streams_kernel<<<(unsigned)blocks, warps_per_block * 32, 0, (cudaStream_t)stream>>>(
+        d_keys, n_streams, n_draws, d_out, ld, log1p_fma, nullptr);
+    return cs::check_launch("exp_streams_kernel");
+}

@@ -1,0 +1,337 @@
+"""JFFC simulation -- CUDA-backed drop-in for chainserve/sim.py.
+
+``run_sim(config) -> SimStats`` keeps the reference signature (sim.py:397) and
+statistics; the replications (RNG streams, event loops, per-rep means and the
+exact order statistics behind the percentiles) run on the GPU through
+``cs_run_sim_host``.  ``run_sim_batch`` simulates many sweep points (e.g. 16
+arrival rates) that share seed/replications in ONE call; each point's
+SimStats is identical to a separate ``run_sim`` call.
+
+Outside the hot path and raising
+NotImplementedError: dedicated-queue policies (jsq/jiq/sed/sa-jsq), sampled
+and trace workloads, and the time-horizon mode.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass
+from typing import Sequence
+
+import numpy as np
+
+from . import _native as N
+from .model import ServerChain, py_sum
+from .workload import PoissonWorkload, SampledWorkload, ServiceTimeModel, TraceWorkload
+
+POLICIES = ("jffc", "jsq", "jiq", "sed", "sa-jsq")
+CENTRAL_QUEUE = None
+
+
+@dataclass(frozen=True)
+class SimConfig:
+    """Simulation knobs; same fields and validation as sim.py:31-72."""
+
+    rates: tuple[float, ...]
+    capacities: tuple[int, ...]
+    workload: PoissonWorkload | SampledWorkload | TraceWorkload
+    policy: str = "jffc"
+    horizon_jobs: int = 100_000
+    horizon_time_s: float | None = None
+    warmup_fraction: float = 0.1
+    seed: int = 1
+    replications: int = 1
+    chains: tuple[ServerChain, ...] | None = None
+    service_model: ServiceTimeModel | None = None
+    collect_jobs: bool = False
+    workers: int = 1
+
+    def __post_init__(self):
+        if self.policy not in POLICIES:
+            raise ValueError(f"unknown policy {self.policy!r}; choose from {POLICIES}")
+        if not self.rates or len(self.rates) != len(self.capacities):
+            raise ValueError("rates and capacities must align and be nonempty")
+        if any(b > a for a, b in zip(self.rates, self.rates[1:])):
+            raise ValueError("rates must be sorted in descending order")
+        if any(c < 1 for c in self.capacities):
+            raise ValueError("capacities must be >= 1")
+        if self.horizon_jobs < 1:
+            raise ValueError("horizon_jobs must be >= 1")
+        if self.horizon_time_s is not None and self.horizon_time_s <= 0:
+            raise ValueError("horizon_time_s must be positive")
+        if not 0.0 <= self.warmup_fraction <= 0.5:
+            raise ValueError("warmup_fraction must lie in [0, 0.5]")
+        if self.replications < 1:
+            raise ValueError("replications must be >= 1")
+        if isinstance(self.workload, TraceWorkload):
+            if self.chains is None or self.service_model is None:
+                raise ValueError("trace workloads need chains and a service-time model")
+            if len(self.chains) != len(self.rates):
+                raise ValueError("one chain object per rate required")
+
+    @property
+    def total_rate(self) -> float:
+        return py_sum(r * c for r, c in zip(self.rates, self.capacities))
+
+
+def policy_step(policy: str, rates: Sequence[float], capacities: Sequence[int],
+                in_service: Sequence[int], queue_lengths: Sequence[int], event: tuple):
+    """Dispatch decision on a snapshot (sim.py:75-117); the GPU event loop
+    inlines the "jffc" branch (first chain with a free slot)."""
+    K = len(rates)
+    kind = event[0]
+    if kind == "completion":
+        k = event[1]
+        backlog = queue_lengths[0] if policy == "jffc" else queue_lengths[k]
+        return k if backlog > 0 else CENTRAL_QUEUE
+    if kind != "arrival":
+        raise ValueError(f"unknown event {event!r}")
+    if policy == "jffc":
+        return next((k for k in range(K) if in_service[k] < capacities[k]), CENTRAL_QUEUE)
+    load = [in_service[k] + queue_lengths[k] for k in range(K)]
+    if policy in ("jsq", "sa-jsq"):
+        return min(range(K), key=lambda k: (load[k], k))
+    if policy == "jiq":
+        for k in range(K):
+            if load[k] < capacities[k]:
+                return k
+        return min(range(K), key=lambda k: (load[k], k))
+    if policy == "sed":
+        return min(range(K), key=lambda k: ((load[k] + 1) / rates[k], k))
+    raise ValueError(f"unknown policy {policy!r}")
+
+
+@dataclass(frozen=True)
+class SimStats:
+    """Aggregated steady-state statistics (sim.py:327-380)."""
+
+    policy: str
+    jobs_counted: int
+    mean_response_s: float
+    median_response_s: float
+    p95_response_s: float
+    p99_response_s: float
+    mean_waiting_s: float
+    mean_service_s: float
+    mean_occupancy: float
+    response_ci_half_width_s: float
+    occupancy_ci_half_width: float
+    per_chain_utilization: tuple[float, ...]
+    lambda_effective: float
+    little_law_gap: float
+    unstable: bool
+    seed: int
+    replications: int
+    rep_mean_response_s: tuple[float, ...]
+    rep_mean_occupancy: tuple[float, ...]
+    occ_first_half: float
+    occ_second_half: float
+    end_queue_len: int
+    job_records: tuple | None = None
+
+    _KEYS = ("policy", "jobs_counted", "mean_response_s", "median_response_s", "p95_response_s",
+             "p99_response_s", "mean_waiting_s", "mean_service_s", "mean_occupancy",
+             "response_ci_half_width_s", "occupancy_ci_half_width", "per_chain_utilization",
+             "lambda_effective", "little_law_gap", "unstable", "seed", "replications",
+             "rep_mean_response_s", "rep_mean_occupancy", "occ_first_half", "occ_second_half",
+             "end_queue_len")
+
+    def to_dict(self) -> dict:
+        d = {k: getattr(self, k) for k in self._KEYS}
+        for k in ("per_chain_utilization", "rep_mean_response_s", "rep_mean_occupancy"):
+            d[k] = list(d[k])
+        return d
+
+
+# ---------------------------------------------------------------------------
+# numpy-exact host arithmetic on the few values the GPU returns
+# ---------------------------------------------------------------------------
+QUANTILES = (0.5, 0.95, 0.99)
+
+
+def _quantile_ranks(n: int, q: float) -> tuple[int, int, float]:
+    """np.quantile(method='linear') neighbours and gamma (numpy _quantile)."""
+    vi = (n - 1) * np.float64(q)
+    prev = math.floor(vi)
+    nxt = prev + 1
+    if vi >= n - 1:
+        prev = nxt = n - 1
+        gamma = float(vi - (-1))  # numpy uses index -1 here; a == b so gamma is irrelevant
+    elif vi < 0:
+        prev = nxt = 0
+        gamma = float(vi - 0)
+    else:
+        gamma = float(vi - prev)
+    return prev, nxt, gamma
+
+
+def _lerp(a: float, b: float, t: float) -> float:
+    """numpy _lerp: a + (b-a)*t, or b - (b-a)*(1-t) when t >= 0.5."""
+    d = b - a
+    return b - d * (1 - t) if t >= 0.5 else a + d * t
+
+
+def _naive_sum(values) -> float:
+    acc = 0.0
+    for x in values:
+        acc = acc + float(x)
+    return acc
+
+
+def _nanmean(values) -> float:
+    x = np.asarray(values, dtype=float)
+    finite = x[~np.isnan(x)]
+    return float(finite.mean()) if finite.size else math.nan
+
+
+def _ci_half_width(values) -> float:
+    from scipy import stats as _st
+
+    x = np.asarray(values, dtype=float)
+    if x.size < 2 or np.any(np.isnan(x)):
+        return math.nan
+    return float(_st.t.ppf(0.975, x.size - 1) * x.std(ddof=1) / math.sqrt(x.size))
+
+
+def _require_supported(cfg: SimConfig) -> None:
+    if cfg.policy != "jffc":
+        raise NotImplementedError(
+            f"policy {cfg.policy!r}: dedicated-queue baselines are a later-round GPU path "
+            "(SURVEY.md §8(f) row 2); the engine simulates 'jffc'")
+    if not isinstance(cfg.workload, PoissonWorkload):
+        raise NotImplementedError("sampled/trace workloads are SURVEY.md §8(f) row 3")
+    if cfg.horizon_time_s is not None:
+        raise NotImplementedError("time-horizon mode is SURVEY.md §8(f) row 4")
+
+
+def _stats_from(cfg: SimConfig, summ: np.ndarray, busy: np.ndarray, order_stats: dict,
+                jobs: np.ndarray | None) -> SimStats:
+    """sim.py:406-456 on per-replication summaries (no response re-reads on host)."""
+    R = cfg.replications
+    counted = int(sum(int(c) for c in summ["counted"]))
+    rep_means = tuple(float(x) for x in summ["resp_mean"])
+    rep_occ = tuple(float(x) for x in summ["mean_occupancy"])
+    # sim.py:410-411 sums np.float64 values, so builtin sum() is the naive
+    # left-to-right sum there (CPython compensates exact floats only)
+    total_wait = _naive_sum(summ["wait_sum"])
+    total_service = _naive_sum(summ["service_sum"])
+    mean_occ = _nanmean(rep_occ)
+    lam_eff = _nanmean([float(x) for x in summ["lambda_effective"]])
+    # merged.mean(): correctly rounded sum of the per-rep pairwise sums
+    mean_resp = math.fsum(float(x) for x in summ["resp_sum"]) / counted
+    caps = cfg.capacities
+    windows = [float(w) for w in summ["window_s"]]
+    util = tuple(
+        _nanmean([float(busy[r, k]) / (caps[k] * windows[r]) if windows[r] > 0 else math.nan
+                  for r in range(R)])
+        for k in range(len(caps)))
+    little = (abs(mean_occ - lam_eff * mean_resp) / mean_occ
+              if mean_occ and not math.isnan(mean_occ) else math.nan)
+    qv = {}
+    for q in QUANTILES:
+        prev, nxt, gamma = _quantile_ranks(counted, q)
+        qv[q] = _lerp(order_stats[prev], order_stats[nxt], gamma)
+    records = None
+    if cfg.collect_jobs and jobs is not None:
+        records = tuple((r, float(a), float(s), float(f), int(k))
+                        for r in range(R) for a, s, f, k in jobs[r])
+    offered = cfg.workload.rate
+    return SimStats(
+        policy=cfg.policy, jobs_counted=counted, mean_response_s=mean_resp,
+        median_response_s=qv[0.5], p95_response_s=qv[0.95], p99_response_s=qv[0.99],
+        mean_waiting_s=total_wait / counted, mean_service_s=total_service / counted,
+        mean_occupancy=mean_occ, response_ci_half_width_s=_ci_half_width(rep_means),
+        occupancy_ci_half_width=_ci_half_width(rep_occ), per_chain_utilization=util,
+        lambda_effective=lam_eff, little_law_gap=little,
+        unstable=bool(offered >= cfg.total_rate), seed=cfg.seed, replications=R,
+        rep_mean_response_s=rep_means, rep_mean_occupancy=rep_occ,
+        occ_first_half=_nanmean([float(x) for x in summ["occ_first_half"]]),
+        occ_second_half=_nanmean([float(x) for x in summ["occ_second_half"]]),
+        end_queue_len=int(max(int(x) for x in summ["end_queue_len"])), job_records=records)
+
+
+@dataclass
+class SweepResult:
+    """Raw device outputs of one batched sweep (point-major rows)."""
+
+    summaries: np.ndarray      # [P, R] SUMMARY_DTYPE
+    busy: np.ndarray           # [P, R, ldb]
+    order_stats: list[dict]    # per point: rank -> value
+    jobs: np.ndarray | None    # [P, R, n, 4]
+    responses: np.ndarray | None = None  # [P, R, n - warm] (completion order)
+
+
+def simulate_sweep(rates_list: Sequence[Sequence[float]], caps_list: Sequence[Sequence[int]],
+                   lams: Sequence[float], n_jobs: int, warmup_fraction: float, seed: int,
+                   replications: int, rep_begin: int = 0, collect_jobs: bool = False,
+                   order_stats: bool = True, max_stream_bytes: int = 8 << 30,
+                   log1p_variant: int = -1, total_replications: int | None = None,
+                   return_responses: bool = False) -> SweepResult:
+    """One GPU call for P points x R replications (all points share the streams
+    of replications rep_begin..rep_begin+R-1 of `seed`)."""
+    lib = N.load()
+    P = len(lams)
+    R = replications
+    warm = int(warmup_fraction * n_jobs)
+    m = n_jobs - warm
+    pts = (N.SimPoint * P)()
+    rates, caps = [], []
+    for p in range(P):
+        pts[p] = N.SimPoint(len(rates_list[p]), len(rates), float(lams[p]))
+        rates.extend(float(x) for x in rates_list[p])
+        caps.extend(int(x) for x in caps_list[p])
+    rates_a = np.asarray(rates, np.float64)
+    caps_a = np.asarray(caps, np.int32)
+    ldb = max(len(r) for r in rates_list)
+    # order statistics needed by np.quantile over the merged responses of each point
+    N_total = (total_replications or R) * m
+    rank_list = sorted({r for q in QUANTILES for r in _quantile_ranks(N_total, q)[:2]})
+    n_ranks = len(rank_list) if order_stats else 0
+    ranks = np.asarray([rank_list] * P, np.int64).ravel() if order_stats else np.zeros(1, np.int64)
+    out_vals = np.zeros(max(P * n_ranks, 1), np.float64)
+    summ = np.zeros(P * R, N.SUMMARY_DTYPE)
+    busy = np.zeros(P * R * ldb, np.float64)
+    jobs = np.zeros(P * R * n_jobs * 4, np.float64) if collect_jobs else None
+    resp = np.zeros(P * R * m, np.float64) if return_responses else None
+    ent = N.seed_words(seed)
+    st = lib.cs_run_sim_host(
+        pts, P, N.ptr(rates_a, C.c_double), N.ptr(caps_a, C.c_int32), len(rates), N.ptr(ent, C.c_uint32),
+        len(ent), rep_begin, R, n_jobs, warm, N.ptr(ranks, C.c_int64) if order_stats else None,
+        n_ranks, log1p_variant, max_stream_bytes, summ.ctypes.data, N.ptr(busy, C.c_double), ldb,
+        N.ptr(out_vals, C.c_double), N.ptr(resp, C.c_double) if resp is not None else None,
+        N.ptr(jobs, C.c_double) if jobs is not None else None, None)
+    N.check(st, "cs_run_sim_host")
+    os_list = [{rank_list[i]: float(out_vals[p * n_ranks + i]) for i in range(n_ranks)}
+               for p in range(P)]
+    return SweepResult(summ.reshape(P, R), busy.reshape(P, R, ldb), os_list,
+                       jobs.reshape(P, R, n_jobs, 4) if jobs is not None else None,
+                       resp.reshape(P, R, m) if resp is not None else None)
+
+
+def run_sim_batch(configs: Sequence[SimConfig]) -> list[SimStats]:
+    """Batched run_sim: configs that differ only in rates/capacities/arrival
+    rate share one GPU call (and their common random number streams)."""
+    if not configs:
+        return []
+    c0 = configs[0]
+    for c in configs:
+        _require_supported(c)
+        if (c.horizon_jobs, c.warmup_fraction, c.seed, c.replications, c.collect_jobs) != \
+                (c0.horizon_jobs, c0.warmup_fraction, c0.seed, c0.replications, c0.collect_jobs):
+            raise ValueError("run_sim_batch: configs must share horizon, warmup, seed, "
+                             "replications and collect_jobs")
+    res = simulate_sweep([c.rates for c in configs], [c.capacities for c in configs],
+                         [c.workload.rate for c in configs], c0.horizon_jobs, c0.warmup_fraction,
+                         c0.seed, c0.replications, collect_jobs=c0.collect_jobs)
+    return [_stats_from(c, res.summaries[p], res.busy[p], res.order_stats[p],
+                        res.jobs[p] if res.jobs is not None else None)
+            for p, c in enumerate(configs)]
+
+
+def run_sim(config: SimConfig) -> SimStats:
+    """All replications on the GPU, aggregated exactly as sim.py:397-456.
+
+    ``workers`` is accepted for signature parity; parallelism is the GPU's.
+    """
+    return run_sim_batch([config])[0]
