@@ -256,7 +256,7 @@ def main():
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms = float(ms_t.item())
     ms_per_step = ms / args.steps
-    value = world * jobs_per_step / (ms / 1e3)
+    value = world * jobs_per_step * args.steps / (ms / 1e3)
 
     sim_ms = float(np.mean([s.sim_ms for s in stage]))
     streams_ms = float(np.mean([s.streams_ms for s in stage]))

@@ -37,6 +37,19 @@ void set_error(const char* fmt, ...) {
     va_end(ap);
 }
 
+void ensure_mem_pool() {
+    static thread_local int done_dev = -1;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return;
+    if (dev == done_dev) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done_dev = dev;
+}
+
 // ---- numpy SeedSequence (bit_generator.pyx), restated for the product ----
 static uint32_t hashmix(uint32_t v, uint32_t& hc) {
     v ^= hc;
@@ -170,6 +183,7 @@ int cs_rep_stats(const double* d_resp, int32_t n_groups, int64_t rows_per_group,
         set_error("cs_rep_stats: no CUDA device");
         return CS_ERR_CUDA;
     }
+    ensure_mem_pool();
     return cs_rep_stats_impl(d_resp, n_groups, rows_per_group, m, ldr, d_summary, ranks, n_ranks,
                              out_values, d_row_sums, stream);
 }
@@ -237,6 +251,7 @@ int cs_run_sim_host(const cs_sim_point* points, int32_t n_points, const double* 
         return CS_ERR_CUDA;
     }
     cudaStream_t st = (cudaStream_t)stream;
+    ensure_mem_pool();
     int rc = CS_OK;
     int32_t max_chains = 1, max_cap = 1;
     for (int p = 0; p < n_points; p++) {

@@ -27,6 +27,10 @@ inline int check_cuda(cudaError_t e, const char* what) {
     return CS_OK;
 }
 
+// Keep freed stream-ordered allocations in the device pool instead of
+// returning them to the OS at every synchronisation (default threshold 0).
+void ensure_mem_pool();
+
 // Python-semantics helpers (no contraction; explicit IEEE round-to-nearest).
 __device__ __forceinline__ double py_div(double a, double b) { return __ddiv_rn(a, b); }
 

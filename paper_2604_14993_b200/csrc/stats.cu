@@ -151,32 +151,36 @@ __global__ void compact_kernel(const double* __restrict__ resp, int64_t n_rows, 
                                const int64_t* __restrict__ grp_off,      // [g][6]
                                unsigned long long* __restrict__ fill,    // [g][6]
                                double* __restrict__ cand) {
-    const int64_t total = n_rows * m;
     const int lane = threadIdx.x & 31;
-    for (int64_t w0 = ((int64_t)blockIdx.x * blockDim.x) & ~31ll; w0 < total;
-         w0 += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t w = w0 + lane + (threadIdx.x & ~31);
-        int list = -1;
-        double v = 0.0;
-        int64_t g = 0;
-        if (w < total) {
-            const int64_t row = w / m;
-            v = resp[row * ldr + (w % m)];
-            g = row / rows_per_group;
-            const uint32_t d0 = (uint32_t)(dbits(v) >> 48);
-            const int nl = grp_nlist[g];
-            for (int q = 0; q < nl; q++)
-                if (grp_bucket[g * 6 + q] == d0) list = (int)(g * 6 + q);
-        }
-        const unsigned active = __ballot_sync(0xffffffffu, list >= 0);
-        if (list >= 0) {
-            const unsigned peers = __match_any_sync(active, list);
-            const int leader = __ffs(peers) - 1;
-            const int rank_in = __popc(peers & ((1u << lane) - 1));
-            unsigned long long base = 0;
-            if (lane == leader) base = atomicAdd(&fill[list], (unsigned long long)__popc(peers));
-            base = __shfl_sync(peers, base, leader);
-            cand[grp_off[list] + (int64_t)base + rank_in] = v;
+    for (int64_t row = blockIdx.x; row < n_rows; row += gridDim.x) {
+        const int64_t g = row / rows_per_group;
+        const int nl = grp_nlist[g];
+        uint32_t bk[6];
+#pragma unroll
+        for (int q = 0; q < 6; q++) bk[q] = q < nl ? grp_bucket[g * 6 + q] : 0xffffffffu;
+        const double* __restrict__ a = resp + row * ldr;
+        // blockDim is a multiple of 32, so every warp runs the same trip count
+        for (int64_t base = 0; base < m; base += blockDim.x) {
+            const int64_t q0 = base + threadIdx.x;
+            int list = -1;
+            double v = 0.0;
+            if (q0 < m) {
+                v = a[q0];
+                const uint32_t d0 = (uint32_t)(dbits(v) >> 48);
+#pragma unroll
+                for (int q = 0; q < 6; q++)
+                    if (bk[q] == d0) list = (int)(g * 6 + q);
+            }
+            const unsigned active = __ballot_sync(0xffffffffu, list >= 0);
+            if (list >= 0) {
+                const unsigned peers = __match_any_sync(active, list);
+                const int leader = __ffs(peers) - 1;
+                const int rank_in = __popc(peers & ((1u << lane) - 1));
+                unsigned long long basei = 0;
+                if (lane == leader) basei = atomicAdd(&fill[list], (unsigned long long)__popc(peers));
+                basei = __shfl_sync(peers, basei, leader);
+                cand[grp_off[list] + (int64_t)basei + rank_in] = v;
+            }
         }
     }
 }
@@ -435,7 +439,7 @@ extern "C" int cs_rep_stats_impl(const double* d_resp, int32_t n_groups, int64_t
     cudaMemcpyAsync(b_off.p, g_off.data(), b_off.n, cudaMemcpyHostToDevice, st);
     cudaMemsetAsync(b_fill.p, 0, b_fill.n, st);
     cudaMemcpyAsync(b_slots.p, slots.data(), b_slots.n, cudaMemcpyHostToDevice, st);
-    compact_kernel<<<sm_count() * 8, 256, 0, st>>>(d_resp, n_rows, m, ldr, rows_per_group,
+    compact_kernel<<<(unsigned)std::min<int64_t>(n_rows, (int64_t)sm_count() * 16), 256, 0, st>>>(d_resp, n_rows, m, ldr, rows_per_group,
                                                    (const int32_t*)b_nl.p, (const uint32_t*)b_bk.p,
                                                    (const int64_t*)b_off.p,
                                                    (unsigned long long*)b_fill.p, (double*)b_cand.p);
