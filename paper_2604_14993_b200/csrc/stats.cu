@@ -1,22 +1,33 @@
-// stats.cu -- run_sim aggregation over the stored responses (sim.py:406-438).
+// stats.cu -- exact order statistics of the merged responses of each sweep
+// point: the values np.quantile interpolates between (sim.py:406,436-438).
 //
-//  * per-replication responses.mean() (sim.py:407) is numpy's pairwise sum
-//    (numpy/_core/src/umath/loops_utils.h.src, @TYPE@_pairwise_sum: blocks of
-//    <=128 summed with 8 accumulators, larger ranges split at n/2 rounded down
-//    to a multiple of 8) divided by the count.  The split tree depends only on
-//    the row length m, so the host builds it once (leaves + post-order
-//    internal nodes) and the device evaluates it: bit-exact with numpy.
-//  * exact order statistics of each sweep point's merged responses (the values
-//    np.quantile interpolates between, sim.py:436-438) by MSB-radix select on
-//    the IEEE bit patterns (responses are >= +0, so bit order == value order):
-//    digit 0 = bits 62..48 (15 bits) histogrammed in the SAME pass as the leaf
-//    sums; then the selected digit-0 buckets are compacted and three 16-bit
-//    digit rounds run on the candidates only.
+// Per replication, responses.mean() (sim.py:407) is numpy's pairwise sum
+// (loops_utils.h.src @TYPE@_pairwise_sum: blocks <= 128 summed with 8
+// accumulators, larger ranges split at n/2 rounded down to a multiple of 8)
+// over the completion-ordered responses / count.  The split tree depends only
+// on the row length m; the host builds it once (leaves + post-order internal
+// nodes) and the device evaluates it bit-exactly: 8 lanes per leaf (lane j =
+// accumulator j), the exact ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) shuffle
+// combine, then a per-row walk of the internal nodes.
+//
+// Quantiles: an exact "sample-select" whose only full read of the responses
+// is fused with the leaf sums above:
+//   1. sample = the first ceil(m/32) responses of every row (contiguous, so
+//      1/32 of the bytes).  Exact order statistics of the sample at ranks
+//      k*|S|/N -+ delta (delta ~ 5 sigma) by MSB radix select on the IEEE bit
+//      patterns (responses are >= +0, so bit order == value order): a 15-bit
+//      digit-0 histogram, compaction of the selected buckets, three 16-bit
+//      digit rounds.  They bracket each target rank: [lo, hi].
+//   2. one coalesced pass over all responses counts, per target, the values
+//      below lo and compacts the values in [lo, hi] (warp-aggregated).
+//   3. if below <= k < below + |candidates| (checked; otherwise the bracket
+//      is widened and step 2 repeats), the k-th value is the (k - below)-th
+//      candidate: four 16-bit digit rounds over the candidates.
 #include <cuda_runtime.h>
+#include <math.h>
+#include <string.h>
 
 #include <algorithm>
-#include <map>
-#include <mutex>
 #include <vector>
 
 #include "cs_internal.cuh"
@@ -26,93 +37,198 @@ namespace cs {
 constexpr int H0_BITS = 15;
 constexpr int H0_BINS = 1 << H0_BITS;
 constexpr int HR_BINS = 1 << 16;
+constexpr int MAX_LISTS = 6;
 
 __device__ __forceinline__ uint64_t dbits(double v) { return (uint64_t)__double_as_longlong(v); }
 
-// Leaf sum exactly as numpy's pairwise_sum for n <= 128.
-__device__ __forceinline__ double leaf_sum(const double* __restrict__ a, int n) {
-    if (n < 8) {
-        double res = 0.0;
-        for (int i = 0; i < n; i++) res = __dadd_rn(res, a[i]);
-        return res;
+int sm_count() {
+    static int n = 0;
+    if (n == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
     }
-    double r0 = a[0], r1 = a[1], r2 = a[2], r3 = a[3], r4 = a[4], r5 = a[5], r6 = a[6], r7 = a[7];
-    int i = 8;
-    const int stop = n - (n % 8);
-    for (; i < stop; i += 8) {
-        const double2 v0 = *reinterpret_cast<const double2*>(a + i);
-        const double2 v1 = *reinterpret_cast<const double2*>(a + i + 2);
-        const double2 v2 = *reinterpret_cast<const double2*>(a + i + 4);
-        const double2 v3 = *reinterpret_cast<const double2*>(a + i + 6);
-        r0 = __dadd_rn(r0, v0.x);
-        r1 = __dadd_rn(r1, v0.y);
-        r2 = __dadd_rn(r2, v1.x);
-        r3 = __dadd_rn(r3, v1.y);
-        r4 = __dadd_rn(r4, v2.x);
-        r5 = __dadd_rn(r5, v2.y);
-        r6 = __dadd_rn(r6, v3.x);
-        r7 = __dadd_rn(r7, v3.y);
-    }
-    double res = __dadd_rn(__dadd_rn(__dadd_rn(r0, r1), __dadd_rn(r2, r3)),
-                           __dadd_rn(__dadd_rn(r4, r5), __dadd_rn(r6, r7)));
-    for (; i < n; i++) res = __dadd_rn(res, a[i]);
-    return res;
+    return n;
 }
 
-// Pass A: leaf sums of every (row, leaf) + digit-0 histogram per group.
-__global__ void __launch_bounds__(1024) leaf_hist_kernel(
-    const double* __restrict__ resp, int64_t n_rows, int64_t ldr, int64_t rows_per_group,
-    const int32_t* __restrict__ leaf_off, const int32_t* __restrict__ leaf_len, int32_t L,
-    double* __restrict__ leaf_sums, uint32_t* __restrict__ hist0, int do_hist,
-    unsigned long long* __restrict__ n_negative) {
-    extern __shared__ uint32_t sh[];  // H0_BINS counters
-    const int64_t total = n_rows * L;
-    const int64_t per_block = (total + gridDim.x - 1) / gridDim.x;
-    const int64_t beg = (int64_t)blockIdx.x * per_block;
-    const int64_t end = min(total, beg + per_block);
-    if (beg >= end) return;
-    const int64_t g_first = (beg / L) / rows_per_group;
-    const int64_t g_last = ((end - 1) / L) / rows_per_group;
-    for (int64_t g = g_first; g <= g_last; g++) {
-        const int64_t gb = max(beg, g * rows_per_group * L);
-        const int64_t ge = min(end, (g + 1) * rows_per_group * L);
-        if (do_hist) {
-            for (int b = threadIdx.x; b < H0_BINS; b += blockDim.x) sh[b] = 0;
-            __syncthreads();
-        }
-        for (int64_t w = gb + threadIdx.x; w < ge; w += blockDim.x) {
-            const int64_t row = w / L;
-            const int leaf = (int)(w % L);
-            const double* a = resp + row * ldr + leaf_off[leaf];
-            const int n = leaf_len[leaf];
-            leaf_sums[w] = leaf_sum(a, n);
-            if (do_hist) {
-                for (int i = 0; i < n; i++) {
-                    const uint64_t u = dbits(a[i]);
-                    if (u >> 63) {
-                        atomicAdd(n_negative, 1ull);
-                    } else {
-                        atomicAdd(&sh[u >> 48], 1u);
-                    }
-                }
+// Digit-0 (bits 62..48) histogram of the first `len` values of every row; a
+// block takes a contiguous range of rows and flushes its shared histogram
+// whenever the group changes.
+__global__ void __launch_bounds__(1024) hist0_rows_kernel(const double* __restrict__ resp, int64_t n_rows,
+                                                          int64_t len, int64_t ldr, int64_t rows_per_group,
+                                                          uint32_t* __restrict__ hist0,
+                                                          unsigned long long* __restrict__ n_bad) {
+    extern __shared__ uint32_t sh[];
+    const int64_t per_block = (n_rows + gridDim.x - 1) / gridDim.x;
+    const int64_t r0 = (int64_t)blockIdx.x * per_block;
+    const int64_t r1 = min(n_rows, r0 + per_block);
+    if (r0 >= r1) return;
+    for (int64_t g = r0 / rows_per_group; g <= (r1 - 1) / rows_per_group; g++) {
+        for (int b = threadIdx.x; b < H0_BINS; b += blockDim.x) sh[b] = 0;
+        __syncthreads();
+        const int64_t ga = max(r0, g * rows_per_group), gb = min(r1, (g + 1) * rows_per_group);
+        for (int64_t row = ga; row < gb; row++) {
+            const double* __restrict__ a = resp + row * ldr;
+            for (int64_t q = threadIdx.x; q < len; q += blockDim.x) {
+                const uint64_t u = dbits(a[q]);
+                if (u >> 63)
+                    atomicAdd(n_bad, 1ull);
+                else
+                    atomicAdd(&sh[u >> 48], 1u);
             }
         }
-        if (do_hist) {
-            __syncthreads();
-            uint32_t* gh = hist0 + g * H0_BINS;
-            for (int b = threadIdx.x; b < H0_BINS; b += blockDim.x)
-                if (sh[b]) atomicAdd(&gh[b], sh[b]);
-            __syncthreads();
+        __syncthreads();
+        uint32_t* gh = hist0 + g * H0_BINS;
+        for (int b = threadIdx.x; b < H0_BINS; b += blockDim.x)
+            if (sh[b]) atomicAdd(&gh[b], sh[b]);
+        __syncthreads();
+    }
+}
+
+// Warp-aggregated append of v to list `list` (all lanes of the warp call it).
+__device__ __forceinline__ void append(int list, double v, unsigned long long* __restrict__ fill,
+                                       const int64_t* __restrict__ off, const int64_t* __restrict__ cap,
+                                       double* __restrict__ cand) {
+    const int lane = threadIdx.x & 31;
+    const unsigned active = __ballot_sync(0xffffffffu, list >= 0);
+    if (list >= 0) {
+        const unsigned peers = __match_any_sync(active, list);
+        const int leader = __ffs(peers) - 1;
+        const int rank_in = __popc(peers & ((1u << lane) - 1));
+        unsigned long long base = 0;
+        if (lane == leader) base = atomicAdd(&fill[list], (unsigned long long)__popc(peers));
+        base = __shfl_sync(peers, base, leader);
+        const int64_t pos = (int64_t)base + rank_in;
+        if (pos < cap[list]) cand[off[list] + pos] = v;  // overflow is detected by the host
+    }
+}
+
+// Sample compaction: values among the first `len` of each row whose digit 0
+// is one of the group's selected buckets.
+__global__ void compact_bucket_kernel(const double* __restrict__ resp, int64_t n_rows, int64_t len,
+                                      int64_t ldr, int64_t rows_per_group,
+                                      const int32_t* __restrict__ grp_nlist,
+                                      const uint32_t* __restrict__ grp_bucket,
+                                      const int64_t* __restrict__ off, const int64_t* __restrict__ cap,
+                                      unsigned long long* __restrict__ fill, double* __restrict__ cand) {
+    for (int64_t row = blockIdx.x; row < n_rows; row += gridDim.x) {
+        const int64_t g = row / rows_per_group;
+        const int nl = grp_nlist[g];
+        uint32_t bk[MAX_LISTS];
+#pragma unroll
+        for (int q = 0; q < MAX_LISTS; q++) bk[q] = q < nl ? grp_bucket[g * MAX_LISTS + q] : 0xffffffffu;
+        const double* __restrict__ a = resp + row * ldr;
+        for (int64_t base = 0; base < len; base += blockDim.x) {
+            const int64_t q0 = base + threadIdx.x;
+            int list = -1;
+            double v = 0.0;
+            if (q0 < len) {
+                v = a[q0];
+                const uint32_t d0 = (uint32_t)(dbits(v) >> 48);
+#pragma unroll
+                for (int q = 0; q < MAX_LISTS; q++)
+                    if (bk[q] == d0) list = (int)(g * MAX_LISTS + q);
+            }
+            append(list, v, fill, off, cap, cand);
         }
     }
 }
 
-// Pass A': combine leaf sums along the split tree (post-order), one thread per row.
+// Leaf sums (numpy pairwise leaves) + bracket counting/compaction, one pass.
+// blockIdx.y = group; warps take 4 leaves at a time (8 lanes per leaf).
+__global__ void __launch_bounds__(256) leaf_bracket_kernel(
+    const double* __restrict__ resp, int64_t rows_per_group, int64_t ldr,
+    const int32_t* __restrict__ leaf_off, const int32_t* __restrict__ leaf_len, int32_t L,
+    double* __restrict__ leaf_sums, int do_bracket, const int32_t* __restrict__ grp_nlist,
+    const uint64_t* __restrict__ lo, const uint64_t* __restrict__ hi, const int64_t* __restrict__ off,
+    const int64_t* __restrict__ cap, unsigned long long* __restrict__ fill,
+    unsigned long long* __restrict__ below, double* __restrict__ cand) {
+    const int64_t g = blockIdx.y;
+    const int lane = threadIdx.x & 31, j = lane & 7, sub = lane >> 3;
+    const int64_t U = rows_per_group * (int64_t)L;  // leaves in this group
+    const int64_t warp_id = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int64_t n_warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const int nl = do_bracket ? grp_nlist[g] : 0;
+    uint64_t bl[MAX_LISTS], bh[MAX_LISTS];
+#pragma unroll
+    for (int q = 0; q < MAX_LISTS; q++) {
+        bl[q] = q < nl ? lo[g * MAX_LISTS + q] : ~0ull;
+        bh[q] = q < nl ? hi[g * MAX_LISTS + q] : 0ull;
+    }
+    uint32_t cnt[MAX_LISTS] = {0, 0, 0, 0, 0, 0};
+    for (int64_t base = warp_id * 4; base < U; base += n_warps * 4) {
+        const int64_t u = base + sub;
+        const bool valid = u < U;
+        const int64_t row = g * rows_per_group + (valid ? u / L : 0);
+        const int leaf = valid ? (int)(u % L) : 0;
+        const double* __restrict__ a = resp + row * ldr + (valid ? leaf_off[leaf] : 0);
+        const int len = valid ? leaf_len[leaf] : 0;
+        const int main_end = len >= 8 ? len - len % 8 : 0;
+        const int steps = __reduce_max_sync(0xffffffffu, (main_end + 7) >> 3);
+        double acc = 0.0;
+        for (int t = 0; t < steps; t++) {
+            const int idx = j + 8 * t;
+            const bool have = idx < main_end;
+            const double v = have ? a[idx] : 0.0;
+            acc = t == 0 ? v : (have ? __dadd_rn(acc, v) : acc);
+            if (do_bracket) {
+                int list = -1;
+                if (have) {
+                    const uint64_t w = dbits(v);
+#pragma unroll
+                    for (int q = 0; q < MAX_LISTS; q++) {
+                        cnt[q] += w < bl[q];
+                        if (w >= bl[q] && w <= bh[q]) list = (int)(g * MAX_LISTS + q);
+                    }
+                }
+                append(list, v, fill, off, cap, cand);
+            }
+        }
+        // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) in numpy's order
+        double s1 = __dadd_rn(acc, __shfl_down_sync(0xffffffffu, acc, 1));
+        double s2 = __dadd_rn(s1, __shfl_down_sync(0xffffffffu, s1, 2));
+        double res = __dadd_rn(s2, __shfl_down_sync(0xffffffffu, s2, 4));
+        // remainder (only the last leaf of a row) / tiny leaves (< 8 values):
+        // lane j == 0 adds them sequentially; every lane joins the warp-wide append
+        const int rem_begin = len >= 8 ? main_end : 0;
+        if (len < 8) res = 0.0;
+        const int rem = __reduce_max_sync(0xffffffffu, len - rem_begin);
+        for (int t = 0; t < rem; t++) {
+            const int idx = rem_begin + t;
+            const bool have = j == 0 && idx < len;
+            const double v = have ? a[idx] : 0.0;
+            if (have) res = __dadd_rn(res, v);
+            if (do_bracket) {
+                int list = -1;
+                if (have) {
+                    const uint64_t w = dbits(v);
+#pragma unroll
+                    for (int q = 0; q < MAX_LISTS; q++) {
+                        cnt[q] += w < bl[q];
+                        if (w >= bl[q] && w <= bh[q]) list = (int)(g * MAX_LISTS + q);
+                    }
+                }
+                append(list, v, fill, off, cap, cand);
+            }
+        }
+        if (valid && j == 0) leaf_sums[(g * rows_per_group) * (int64_t)L + u] = res;
+    }
+    if (do_bracket) {
+#pragma unroll
+        for (int q = 0; q < MAX_LISTS; q++) {
+            uint32_t c = cnt[q];
+            for (int d = 16; d > 0; d >>= 1) c += __shfl_down_sync(0xffffffffu, c, d);
+            if (lane == 0 && q < nl && c) atomicAdd(&below[g * MAX_LISTS + q], (unsigned long long)c);
+        }
+    }
+}
+
+// Internal nodes of the split tree, post-order, one thread per row.
 __global__ void tree_combine_kernel(const double* __restrict__ leaf_sums, int32_t L,
                                     const int32_t* __restrict__ node_l, const int32_t* __restrict__ node_r,
-                                    int32_t n_nodes, double* __restrict__ scratch, int64_t n_rows,
-                                    int64_t m, cs_rep_summary* __restrict__ summ,
-                                    double* __restrict__ row_sums) {
+                                    int32_t n_nodes, double* __restrict__ scratch, int64_t n_rows, int64_t m,
+                                    cs_rep_summary* __restrict__ summ, double* __restrict__ row_sums) {
     const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (row >= n_rows) return;
     const double* ls = leaf_sums + row * L;
@@ -132,67 +248,19 @@ __global__ void tree_combine_kernel(const double* __restrict__ leaf_sums, int32_
     }
 }
 
-// Per-slot selection state.
 struct SelSlot {
-    uint64_t prefix;   // selected high bits so far (already shifted into place)
-    int64_t rank;      // remaining rank within the candidates with that prefix
-    int64_t cand_off;  // candidate list offset / length
+    uint64_t prefix;   // selected high bits so far
+    int64_t rank;      // remaining rank among the candidates sharing the prefix
+    int64_t cand_off;  // candidate list
     int64_t cand_len;
-    int32_t group;
-    int32_t list;      // candidate list id
 };
 
-// Pass B: compact the values of each group whose digit 0 equals one of the
-// group's selected buckets (lists are distinct per (group, bucket)).
-__global__ void compact_kernel(const double* __restrict__ resp, int64_t n_rows, int64_t m,
-                               int64_t ldr, int64_t rows_per_group,
-                               const int32_t* __restrict__ grp_nlist,
-                               const uint32_t* __restrict__ grp_bucket,  // [g][6]
-                               const int64_t* __restrict__ grp_off,      // [g][6]
-                               unsigned long long* __restrict__ fill,    // [g][6]
-                               double* __restrict__ cand) {
-    const int lane = threadIdx.x & 31;
-    for (int64_t row = blockIdx.x; row < n_rows; row += gridDim.x) {
-        const int64_t g = row / rows_per_group;
-        const int nl = grp_nlist[g];
-        uint32_t bk[6];
-#pragma unroll
-        for (int q = 0; q < 6; q++) bk[q] = q < nl ? grp_bucket[g * 6 + q] : 0xffffffffu;
-        const double* __restrict__ a = resp + row * ldr;
-        // blockDim is a multiple of 32, so every warp runs the same trip count
-        for (int64_t base = 0; base < m; base += blockDim.x) {
-            const int64_t q0 = base + threadIdx.x;
-            int list = -1;
-            double v = 0.0;
-            if (q0 < m) {
-                v = a[q0];
-                const uint32_t d0 = (uint32_t)(dbits(v) >> 48);
-#pragma unroll
-                for (int q = 0; q < 6; q++)
-                    if (bk[q] == d0) list = (int)(g * 6 + q);
-            }
-            const unsigned active = __ballot_sync(0xffffffffu, list >= 0);
-            if (list >= 0) {
-                const unsigned peers = __match_any_sync(active, list);
-                const int leader = __ffs(peers) - 1;
-                const int rank_in = __popc(peers & ((1u << lane) - 1));
-                unsigned long long basei = 0;
-                if (lane == leader) basei = atomicAdd(&fill[list], (unsigned long long)__popc(peers));
-                basei = __shfl_sync(peers, basei, leader);
-                cand[grp_off[list] + (int64_t)basei + rank_in] = v;
-            }
-        }
-    }
-}
-
-// Rounds 1..3: histogram of the 16-bit digit at `shift` over candidates whose
-// bits above the digit equal the slot prefix.
 __global__ void round_hist_kernel(const double* __restrict__ cand, const SelSlot* __restrict__ slots,
                                   int n_slots, int shift, uint32_t* __restrict__ hist) {
     const int s = blockIdx.y;
     if (s >= n_slots) return;
     const SelSlot sl = slots[s];
-    const uint64_t hi_mask = ~((1ull << (shift + 16)) - 1);
+    const uint64_t hi_mask = shift + 16 >= 64 ? 0ull : ~((1ull << (shift + 16)) - 1);
     uint32_t* h = hist + (int64_t)s * HR_BINS;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < sl.cand_len;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -201,7 +269,6 @@ __global__ void round_hist_kernel(const double* __restrict__ cand, const SelSlot
     }
 }
 
-// Select the bucket holding `rank` in each slot's histogram; one block per slot.
 __global__ void __launch_bounds__(1024) round_select_kernel(SelSlot* __restrict__ slots, int n_slots,
                                                             int shift, const uint32_t* __restrict__ hist) {
     const int s = blockIdx.x;
@@ -213,7 +280,6 @@ __global__ void __launch_bounds__(1024) round_select_kernel(SelSlot* __restrict_
     for (int b = threadIdx.x * per; b < (threadIdx.x + 1) * per; b++) acc += h[b];
     part[threadIdx.x] = acc;
     __syncthreads();
-    // inclusive scan (Hillis-Steele) over partials
     for (int d = 1; d < (int)blockDim.x; d <<= 1) {
         unsigned long long v = threadIdx.x >= (unsigned)d ? part[threadIdx.x - d] : 0ull;
         __syncthreads();
@@ -238,239 +304,350 @@ __global__ void __launch_bounds__(1024) round_select_kernel(SelSlot* __restrict_
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
+struct DBuf {
+    void* p = nullptr;
+    size_t n = 0;
+    cudaStream_t st = nullptr;
+    ~DBuf() {
+        if (p) cudaFreeAsync(p, st);
+    }
+    int alloc(size_t bytes, cudaStream_t s) {
+        st = s;
+        n = bytes;
+        return check_cuda(cudaMallocAsync(&p, bytes ? bytes : 16, s), "cudaMallocAsync");
+    }
+    template <class T>
+    T* as() const {
+        return (T*)p;
+    }
+};
+
+static uint64_t bits_of(double d) {
+    uint64_t u;
+    memcpy(&u, &d, 8);
+    return u;
+}
+
+// Exact values for `slots` (prefix/rank preset) from candidate lists: 16-bit
+// digit rounds from bit `first_shift` down to 0.
+static int run_rounds(std::vector<SelSlot>& slots, const double* d_cand, int first_shift, cudaStream_t st) {
+    const int n_slots = (int)slots.size();
+    if (n_slots == 0) return CS_OK;
+    DBuf b_slots, b_hist;
+    int rc;
+    if ((rc = b_slots.alloc(sizeof(SelSlot) * n_slots, st)) ||
+        (rc = b_hist.alloc(sizeof(uint32_t) * HR_BINS * (size_t)n_slots, st)))
+        return rc;
+    cudaMemcpyAsync(b_slots.p, slots.data(), b_slots.n, cudaMemcpyHostToDevice, st);
+    for (int shift = first_shift; shift >= 0; shift -= 16) {
+        cudaMemsetAsync(b_hist.p, 0, b_hist.n, st);
+        dim3 grid(std::max(1, sm_count() * 4 / n_slots), n_slots);
+        round_hist_kernel<<<grid, 256, 0, st>>>(d_cand, b_slots.as<SelSlot>(), n_slots, shift,
+                                                b_hist.as<uint32_t>());
+        if ((rc = check_launch("round_hist_kernel"))) return rc;
+        round_select_kernel<<<n_slots, 1024, 0, st>>>(b_slots.as<SelSlot>(), n_slots, shift,
+                                                      b_hist.as<uint32_t>());
+        if ((rc = check_launch("round_select_kernel"))) return rc;
+    }
+    cudaMemcpyAsync(slots.data(), b_slots.p, b_slots.n, cudaMemcpyDeviceToHost, st);
+    return check_cuda(cudaStreamSynchronize(st), "rounds sync");
+}
+
+// Exact order statistics over the first `len` values of every row (groups of
+// rows_per_group rows); ranks: n_groups x n_ranks, 0-based.
+static int select_rows(const double* d_resp, int64_t n_groups, int64_t rows_per_group, int64_t len,
+                       int64_t ldr, const std::vector<int64_t>& ranks, int n_ranks, std::vector<double>& out,
+                       cudaStream_t st) {
+    const int64_t n_rows = n_groups * rows_per_group;
+    int rc;
+    DBuf b_h0, b_bad;
+    if ((rc = b_h0.alloc(sizeof(uint32_t) * H0_BINS * (size_t)n_groups, st)) ||
+        (rc = b_bad.alloc(sizeof(unsigned long long), st)))
+        return rc;
+    cudaMemsetAsync(b_h0.p, 0, b_h0.n, st);
+    cudaMemsetAsync(b_bad.p, 0, b_bad.n, st);
+    const size_t smem = sizeof(uint32_t) * H0_BINS;
+    cudaFuncSetAttribute(hist0_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const int blocks = (int)std::min<int64_t>(n_rows, sm_count());
+    hist0_rows_kernel<<<blocks, 1024, smem, st>>>(d_resp, n_rows, len, ldr, rows_per_group,
+                                                  b_h0.as<uint32_t>(), b_bad.as<unsigned long long>());
+    if ((rc = check_launch("hist0_rows_kernel"))) return rc;
+    std::vector<uint32_t> h0((size_t)H0_BINS * n_groups);
+    unsigned long long bad = 0;
+    cudaMemcpyAsync(h0.data(), b_h0.p, b_h0.n, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(&bad, b_bad.p, sizeof(bad), cudaMemcpyDeviceToHost, st);
+    if ((rc = check_cuda(cudaStreamSynchronize(st), "select hist sync"))) return rc;
+    if (bad) {
+        set_error("cs_rep_stats: %llu negative responses (impossible for valid input)", bad);
+        return CS_INTERNAL;
+    }
+    std::vector<int32_t> nlist(n_groups, 0);
+    std::vector<uint32_t> bucket((size_t)n_groups * MAX_LISTS, 0xffffffffu);
+    std::vector<int64_t> off((size_t)n_groups * MAX_LISTS, 0), cap((size_t)n_groups * MAX_LISTS, 0);
+    std::vector<SelSlot> slots((size_t)n_groups * n_ranks);
+    int64_t total = 0;
+    for (int64_t g = 0; g < n_groups; g++) {
+        const uint32_t* hg = h0.data() + (size_t)g * H0_BINS;
+        for (int q = 0; q < n_ranks; q++) {
+            const int64_t rank = ranks[g * n_ranks + q];
+            int64_t c = 0;
+            uint32_t b = 0;
+            for (; b < (uint32_t)H0_BINS; b++) {
+                if (c + (int64_t)hg[b] > rank) break;
+                c += hg[b];
+            }
+            int list = -1;
+            for (int l = 0; l < nlist[g]; l++)
+                if (bucket[g * MAX_LISTS + l] == b) list = l;
+            if (list < 0) {
+                list = nlist[g]++;
+                bucket[g * MAX_LISTS + list] = b;
+                off[g * MAX_LISTS + list] = total;
+                cap[g * MAX_LISTS + list] = hg[b];
+                total += hg[b];
+            }
+            SelSlot& s = slots[g * n_ranks + q];
+            s.prefix = (uint64_t)b << 48;
+            s.rank = rank - c;
+            s.cand_off = off[g * MAX_LISTS + list];
+            s.cand_len = cap[g * MAX_LISTS + list];
+        }
+    }
+    DBuf b_nl, b_bk, b_off, b_cap, b_fill, b_cand;
+    if ((rc = b_nl.alloc(sizeof(int32_t) * n_groups, st)) ||
+        (rc = b_bk.alloc(sizeof(uint32_t) * MAX_LISTS * n_groups, st)) ||
+        (rc = b_off.alloc(sizeof(int64_t) * MAX_LISTS * n_groups, st)) ||
+        (rc = b_cap.alloc(sizeof(int64_t) * MAX_LISTS * n_groups, st)) ||
+        (rc = b_fill.alloc(sizeof(unsigned long long) * MAX_LISTS * n_groups, st)) ||
+        (rc = b_cand.alloc(sizeof(double) * std::max<int64_t>(total, 1), st)))
+        return rc;
+    cudaMemcpyAsync(b_nl.p, nlist.data(), b_nl.n, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(b_bk.p, bucket.data(), b_bk.n, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(b_off.p, off.data(), b_off.n, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(b_cap.p, cap.data(), b_cap.n, cudaMemcpyHostToDevice, st);
+    cudaMemsetAsync(b_fill.p, 0, b_fill.n, st);
+    compact_bucket_kernel<<<(unsigned)std::min<int64_t>(n_rows, (int64_t)sm_count() * 16), 256, 0, st>>>(
+        d_resp, n_rows, len, ldr, rows_per_group, b_nl.as<int32_t>(), b_bk.as<uint32_t>(),
+        b_off.as<int64_t>(), b_cap.as<int64_t>(), b_fill.as<unsigned long long>(), b_cand.as<double>());
+    if ((rc = check_launch("compact_bucket_kernel"))) return rc;
+    if ((rc = run_rounds(slots, b_cand.as<double>(), 32, st))) return rc;  // bits 47..0
+    out.resize(slots.size());
+    for (size_t i = 0; i < slots.size(); i++) memcpy(&out[i], &slots[i].prefix, 8);
+    return CS_OK;
+}
+
+// Split tree of numpy's pairwise sum for rows of m values (cached per m).
 struct PairwisePlan {
+    int64_t m = -1;
     std::vector<int32_t> leaf_off, leaf_len, node_l, node_r;
 };
 
-static int32_t build_plan(PairwisePlan& pl, int64_t off, int64_t n) {
+static int32_t plan_build(PairwisePlan& pl, int64_t off, int64_t n) {
     if (n <= 128) {
         pl.leaf_off.push_back((int32_t)off);
         pl.leaf_len.push_back((int32_t)n);
-        return (int32_t)(pl.leaf_off.size() - 1);
+        return (int32_t)pl.leaf_off.size() - 1;
     }
     int64_t n2 = n / 2;
     n2 -= n2 % 8;
-    const int32_t a = build_plan(pl, off, n2);
-    const int32_t b = build_plan(pl, off + n2, n - n2);
+    const int32_t a = plan_build(pl, off, n2);
+    const int32_t b = plan_build(pl, off + n2, n - n2);
     pl.node_l.push_back(a);
     pl.node_r.push_back(b);
-    return -(int32_t)pl.node_l.size();  // internal: encoded below
+    return -(int32_t)pl.node_l.size();  // internal node q encoded as -(q+1)
 }
 
-// Node ids: leaves 0..L-1, internal node q -> L + q.  build_plan returns
-// negative ids for internal nodes; fix them up after the leaf count is known.
-static PairwisePlan make_plan(int64_t m) {
-    PairwisePlan pl;
-    std::vector<int32_t> dummy;
-    if (m <= 0) return pl;
-    build_plan(pl, 0, m);
-    const int32_t L = (int32_t)pl.leaf_off.size();
-    for (auto& x : pl.node_l)
-        if (x < 0) x = L + (-x - 1);
-    for (auto& x : pl.node_r)
-        if (x < 0) x = L + (-x - 1);
-    return pl;
-}
-
-struct Buf {
-    void* p = nullptr;
-    size_t n = 0;
-};
-
-static int dmalloc(Buf& b, size_t bytes, cudaStream_t st) {
-    b.n = bytes;
-    if (bytes == 0) return CS_OK;
-    return check_cuda(cudaMallocAsync(&b.p, bytes, st), "cudaMallocAsync");
-}
-static void dfree(Buf& b, cudaStream_t st) {
-    if (b.p) cudaFreeAsync(b.p, st);
-    b.p = nullptr;
-}
-
-int sm_count() {
-    static int n = 0;
-    if (n == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-        if (n <= 0) n = 148;
+static const PairwisePlan& pairwise_plan(int64_t m) {
+    static thread_local PairwisePlan pl;
+    if (pl.m != m) {
+        pl = PairwisePlan();
+        pl.m = m;
+        if (m > 0) plan_build(pl, 0, m);
+        const int32_t L = (int32_t)pl.leaf_off.size();
+        for (auto* v : {&pl.node_l, &pl.node_r})
+            for (auto& x : *v)
+                if (x < 0) x = L + (-x - 1);
     }
-    return n;
+    return pl;
 }
 
 }  // namespace cs
 
 using namespace cs;
 
-// Per-row numpy pairwise sums -> summ[row].resp_mean (and row_sums if given);
-// optionally the digit-0 histogram (for the rank selection).
-static int row_stats(const double* d_resp, int64_t n_rows, int64_t m, int64_t ldr,
-                     int64_t rows_per_group, cs_rep_summary* d_summ, double* d_row_sums,
-                     uint32_t* d_hist0, unsigned long long* d_neg, cudaStream_t st) {
-    const PairwisePlan pl = make_plan(m);
-    const int32_t L = (int32_t)pl.leaf_off.size();
-    const int32_t NN = (int32_t)pl.node_l.size();
-    Buf b_lo, b_ll, b_nl, b_nr, b_ls, b_sc;
-    int rc = CS_OK;
-    if ((rc = dmalloc(b_lo, sizeof(int32_t) * L, st)) || (rc = dmalloc(b_ll, sizeof(int32_t) * L, st)) ||
-        (rc = dmalloc(b_nl, sizeof(int32_t) * (NN + 1), st)) ||
-        (rc = dmalloc(b_nr, sizeof(int32_t) * (NN + 1), st)) ||
-        (rc = dmalloc(b_ls, sizeof(double) * (size_t)n_rows * L, st)) ||
-        (rc = dmalloc(b_sc, sizeof(double) * (size_t)n_rows * (NN > 0 ? NN : 1), st)))
-        return rc;
-    cudaMemcpyAsync(b_lo.p, pl.leaf_off.data(), sizeof(int32_t) * L, cudaMemcpyHostToDevice, st);
-    cudaMemcpyAsync(b_ll.p, pl.leaf_len.data(), sizeof(int32_t) * L, cudaMemcpyHostToDevice, st);
-    if (NN) {
-        cudaMemcpyAsync(b_nl.p, pl.node_l.data(), sizeof(int32_t) * NN, cudaMemcpyHostToDevice, st);
-        cudaMemcpyAsync(b_nr.p, pl.node_r.data(), sizeof(int32_t) * NN, cudaMemcpyHostToDevice, st);
-    }
-    const size_t smem = d_hist0 ? sizeof(uint32_t) * H0_BINS : 0;
-    if (smem) cudaFuncSetAttribute(leaf_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    const int64_t work = n_rows * L;
-    int blocks = sm_count();
-    if (work < (int64_t)blocks * 256) blocks = (int)std::max<int64_t>(1, (work + 255) / 256);
-    leaf_hist_kernel<<<blocks, 1024, smem, st>>>(d_resp, n_rows, ldr, rows_per_group,
-                                                 (const int32_t*)b_lo.p, (const int32_t*)b_ll.p, L,
-                                                 (double*)b_ls.p, d_hist0, d_hist0 != nullptr, d_neg);
-    if ((rc = check_launch("leaf_hist_kernel"))) return rc;
-    tree_combine_kernel<<<(unsigned)((n_rows + 127) / 128), 128, 0, st>>>(
-        (const double*)b_ls.p, L, (const int32_t*)b_nl.p, (const int32_t*)b_nr.p, NN, (double*)b_sc.p,
-        n_rows, m, d_summ, d_row_sums);
-    if ((rc = check_launch("tree_combine_kernel"))) return rc;
-    dfree(b_lo, st);
-    dfree(b_ll, st);
-    dfree(b_nl, st);
-    dfree(b_nr, st);
-    dfree(b_ls, st);
-    dfree(b_sc, st);
-    return CS_OK;
-}
-
-extern "C" int cs_rep_stats_impl(const double* d_resp, int32_t n_groups, int64_t rows_per_group,
-                                 int64_t m, int64_t ldr, cs_rep_summary* d_summ,
-                                 const int64_t* ranks, int32_t n_ranks, double* out_values,
-                                 double* d_row_sums, void* stream) {
+extern "C" int cs_rep_stats_impl(const double* d_resp, int32_t n_groups, int64_t rows_per_group, int64_t m,
+                                 int64_t ldr, cs_rep_summary* d_summ, const int64_t* ranks,
+                                 int32_t n_ranks, double* out_values, double* d_row_sums, void* stream) {
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t n_rows = (int64_t)n_groups * rows_per_group;
     if (n_rows == 0 || m == 0) return CS_OK;
-    if (n_ranks > 6) {
-        set_error("cs_rep_stats: at most 6 ranks per group");
+    if (ranks != nullptr && n_ranks > MAX_LISTS) {
+        set_error("cs_rep_stats: at most %d ranks per group", MAX_LISTS);
         return CS_INVALID;
     }
-    const bool select = ranks != nullptr && n_ranks > 0;
-    Buf b_h0, b_neg;
-    int rc = CS_OK;
-    if (select) {
-        if ((rc = dmalloc(b_h0, sizeof(uint32_t) * H0_BINS * (size_t)n_groups, st)) ||
-            (rc = dmalloc(b_neg, sizeof(unsigned long long), st)))
-            return rc;
-        cudaMemsetAsync(b_h0.p, 0, b_h0.n, st);
-        cudaMemsetAsync(b_neg.p, 0, b_neg.n, st);
-    }
-    rc = row_stats(d_resp, n_rows, m, ldr, rows_per_group, d_summ, d_row_sums,
-                   (uint32_t*)b_h0.p, (unsigned long long*)b_neg.p, st);
-    if (rc || !select) {
-        dfree(b_h0, st);
-        dfree(b_neg, st);
-        return rc;
-    }
-    // ---- digit 0 selection on the host (2 MB for 16 groups) ----
-    std::vector<uint32_t> h0((size_t)H0_BINS * n_groups);
-    unsigned long long neg = 0;
-    cudaMemcpyAsync(h0.data(), b_h0.p, b_h0.n, cudaMemcpyDeviceToHost, st);
-    cudaMemcpyAsync(&neg, b_neg.p, sizeof(neg), cudaMemcpyDeviceToHost, st);
-    if ((rc = check_cuda(cudaStreamSynchronize(st), "rep_stats sync"))) return rc;
-    if (neg) {
-        set_error("cs_rep_stats: %llu negative responses (impossible for valid input)", neg);
-        return CS_INTERNAL;
-    }
-    const int64_t n_vals = rows_per_group * m;
-    std::vector<SelSlot> slots((size_t)n_groups * n_ranks);
-    std::vector<int32_t> g_nlist(n_groups, 0);
-    std::vector<uint32_t> g_bucket((size_t)n_groups * 6, 0xffffffffu);
-    std::vector<int64_t> g_off((size_t)n_groups * 6, 0), g_len((size_t)n_groups * 6, 0);
-    int64_t total_cand = 0;
-    for (int g = 0; g < n_groups; g++) {
-        const uint32_t* hg = h0.data() + (size_t)g * H0_BINS;
-        for (int q = 0; q < n_ranks; q++) {
-            int64_t rank = ranks[(size_t)g * n_ranks + q];
-            if (rank < 0) rank += n_vals;
-            if (rank < 0 || rank >= n_vals) {
-                set_error("cs_rep_stats: rank out of range");
-                return CS_INVALID;
-            }
-            int64_t c = 0;
-            uint32_t b = 0;
-            for (; b < (uint32_t)H0_BINS; b++) {
-                if (c + hg[b] > (uint64_t)rank) break;
-                c += hg[b];
-            }
-            int list = -1;
-            for (int l = 0; l < g_nlist[g]; l++)
-                if (g_bucket[g * 6 + l] == b) list = l;
-            if (list < 0) {
-                list = g_nlist[g]++;
-                g_bucket[g * 6 + list] = b;
-                g_off[g * 6 + list] = total_cand;
-                g_len[g * 6 + list] = hg[b];
-                total_cand += hg[b];
-            }
-            SelSlot& s = slots[(size_t)g * n_ranks + q];
-            s.prefix = (uint64_t)b << 48;
-            s.rank = rank - c;
-            s.cand_off = g_off[g * 6 + list];
-            s.cand_len = g_len[g * 6 + list];
-            s.group = g;
-            s.list = g * 6 + list;
+    const bool want_ranks = ranks != nullptr && n_ranks > 0;
+    const int64_t N = rows_per_group * m;  // values per group
+    std::vector<int64_t> target(want_ranks ? (size_t)n_groups * n_ranks : 0);
+    for (size_t i = 0; i < target.size(); i++) {
+        int64_t k = ranks[i];
+        if (k < 0) k += N;
+        if (k < 0 || k >= N) {
+            set_error("cs_rep_stats: rank out of range");
+            return CS_INVALID;
         }
+        target[i] = k;
     }
-    Buf b_nl, b_bk, b_off, b_fill, b_cand, b_slots, b_hist;
-    const int n_slots = (int)slots.size();
-    if ((rc = dmalloc(b_nl, sizeof(int32_t) * n_groups, st)) ||
-        (rc = dmalloc(b_bk, sizeof(uint32_t) * 6 * n_groups, st)) ||
-        (rc = dmalloc(b_off, sizeof(int64_t) * 6 * n_groups, st)) ||
-        (rc = dmalloc(b_fill, sizeof(unsigned long long) * 6 * n_groups, st)) ||
-        (rc = dmalloc(b_cand, sizeof(double) * (size_t)std::max<int64_t>(total_cand, 1), st)) ||
-        (rc = dmalloc(b_slots, sizeof(SelSlot) * n_slots, st)) ||
-        (rc = dmalloc(b_hist, sizeof(uint32_t) * HR_BINS * (size_t)n_slots, st)))
+    int rc;
+    // ---- pairwise plan + scratch ----
+    const PairwisePlan& pl = pairwise_plan(m);
+    const int32_t L = (int32_t)pl.leaf_off.size();
+    const int32_t NN = (int32_t)pl.node_l.size();
+    DBuf b_plan, b_ls, b_sc;
+    if ((rc = b_plan.alloc(sizeof(int32_t) * (2 * (size_t)L + 2 * (size_t)NN + 2), st)) ||
+        (rc = b_ls.alloc(sizeof(double) * (size_t)n_rows * L, st)) ||
+        (rc = b_sc.alloc(sizeof(double) * (size_t)n_rows * std::max(NN, 1), st)))
         return rc;
-    cudaMemcpyAsync(b_nl.p, g_nlist.data(), b_nl.n, cudaMemcpyHostToDevice, st);
-    cudaMemcpyAsync(b_bk.p, g_bucket.data(), b_bk.n, cudaMemcpyHostToDevice, st);
-    cudaMemcpyAsync(b_off.p, g_off.data(), b_off.n, cudaMemcpyHostToDevice, st);
-    cudaMemsetAsync(b_fill.p, 0, b_fill.n, st);
-    cudaMemcpyAsync(b_slots.p, slots.data(), b_slots.n, cudaMemcpyHostToDevice, st);
-    compact_kernel<<<(unsigned)std::min<int64_t>(n_rows, (int64_t)sm_count() * 16), 256, 0, st>>>(d_resp, n_rows, m, ldr, rows_per_group,
-                                                   (const int32_t*)b_nl.p, (const uint32_t*)b_bk.p,
-                                                   (const int64_t*)b_off.p,
-                                                   (unsigned long long*)b_fill.p, (double*)b_cand.p);
-    if ((rc = check_launch("compact_kernel"))) return rc;
-    for (int round = 1; round <= 3; round++) {
-        const int shift = 48 - 16 * round;
-        cudaMemsetAsync(b_hist.p, 0, b_hist.n, st);
-        dim3 grid(std::max(1, sm_count() * 4 / std::max(1, n_slots)), n_slots);
-        round_hist_kernel<<<grid, 256, 0, st>>>((const double*)b_cand.p, (const SelSlot*)b_slots.p,
-                                                n_slots, shift, (uint32_t*)b_hist.p);
-        if ((rc = check_launch("round_hist_kernel"))) return rc;
-        round_select_kernel<<<n_slots, 1024, 0, st>>>((SelSlot*)b_slots.p, n_slots, shift,
-                                                      (const uint32_t*)b_hist.p);
-        if ((rc = check_launch("round_select_kernel"))) return rc;
+    int32_t* d_lo_off = b_plan.as<int32_t>();
+    int32_t* d_lo_len = d_lo_off + L;
+    int32_t* d_nl = d_lo_len + L;
+    int32_t* d_nr = d_nl + NN + 1;
+    cudaMemcpyAsync(d_lo_off, pl.leaf_off.data(), sizeof(int32_t) * L, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(d_lo_len, pl.leaf_len.data(), sizeof(int32_t) * L, cudaMemcpyHostToDevice, st);
+    if (NN) {
+        cudaMemcpyAsync(d_nl, pl.node_l.data(), sizeof(int32_t) * NN, cudaMemcpyHostToDevice, st);
+        cudaMemcpyAsync(d_nr, pl.node_r.data(), sizeof(int32_t) * NN, cudaMemcpyHostToDevice, st);
     }
-    cudaMemcpyAsync(slots.data(), b_slots.p, b_slots.n, cudaMemcpyDeviceToHost, st);
-    rc = check_cuda(cudaStreamSynchronize(st), "rep_stats select sync");
-    for (int s = 0; s < n_slots && rc == CS_OK; s++) {
-        uint64_t u = slots[s].prefix;
-        double v;
-        memcpy(&v, &u, 8);
-        out_values[s] = v;
+    const int64_t U = rows_per_group * (int64_t)L;
+    const int bx = (int)std::max<int64_t>(1, std::min<int64_t>((U + 31) / 32, (int64_t)sm_count() * 8 / n_groups + 1));
+    auto leaf_pass = [&](int do_bracket, const int32_t* nl, const uint64_t* lo, const uint64_t* hi,
+                         const int64_t* off, const int64_t* cap, unsigned long long* fill,
+                         unsigned long long* below, double* cand) {
+        dim3 grid(bx, n_groups);
+        leaf_bracket_kernel<<<grid, 256, 0, st>>>(d_resp, rows_per_group, ldr, d_lo_off, d_lo_len, L,
+                                                  b_ls.as<double>(), do_bracket, nl, lo, hi, off, cap, fill,
+                                                  below, cand);
+        return check_launch("leaf_bracket_kernel");
+    };
+    auto combine = [&]() {
+        tree_combine_kernel<<<(unsigned)((n_rows + 127) / 128), 128, 0, st>>>(
+            b_ls.as<double>(), L, d_nl, d_nr, NN, b_sc.as<double>(), n_rows, m, d_summ, d_row_sums);
+        return check_launch("tree_combine_kernel");
+    };
+    const int64_t ms = (m + 31) / 32;
+    if (!want_ranks || N <= (1 << 20) || ms < 8) {
+        if ((rc = leaf_pass(0, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr)) ||
+            (rc = combine()))
+            return rc;
+        if (!want_ranks) return CS_OK;
+        std::vector<double> vals;  // small groups: exact selection over all values
+        if ((rc = select_rows(d_resp, n_groups, rows_per_group, m, ldr, target, n_ranks, vals, st))) return rc;
+        for (size_t i = 0; i < vals.size(); i++) out_values[i] = vals[i];
+        return CS_OK;
     }
-    dfree(b_h0, st);
-    dfree(b_neg, st);
-    dfree(b_nl, st);
-    dfree(b_bk, st);
-    dfree(b_off, st);
-    dfree(b_fill, st);
-    dfree(b_cand, st);
-    dfree(b_slots, st);
-    dfree(b_hist, st);
-    return rc;
+    const int64_t NS = rows_per_group * ms;  // sample size per group
+    const size_t T = target.size();
+    bool combined = false;
+    double widen = 1.0;
+    for (int attempt = 0; attempt < 4; attempt++, widen *= 8.0) {
+        // ---- 1. sample order statistics bracketing each target ----
+        std::vector<int64_t> r_lo(T), r_hi(T);
+        for (size_t i = 0; i < T; i++) {
+            const double p = (double)target[i] / (double)N;
+            const double ks = p * (double)NS;
+            const double delta = widen * (5.0 * sqrt(ks * (1.0 - p) + 1.0) + 16.0);
+            r_lo[i] = std::max<int64_t>(0, (int64_t)floor(ks - delta));
+            r_hi[i] = std::min<int64_t>(NS - 1, (int64_t)ceil(ks + delta));
+        }
+        std::vector<double> v_lo, v_hi;
+        if ((rc = select_rows(d_resp, n_groups, rows_per_group, ms, ldr, r_lo, n_ranks, v_lo, st)) ||
+            (rc = select_rows(d_resp, n_groups, rows_per_group, ms, ldr, r_hi, n_ranks, v_hi, st)))
+            return rc;
+        std::vector<int32_t> nlist(n_groups, 0);
+        const size_t L6 = (size_t)n_groups * MAX_LISTS;
+        std::vector<uint64_t> lo(L6, ~0ull), hi(L6, 0);
+        std::vector<int> list_of(T);
+        std::vector<int64_t> est(L6, 0);
+        for (int64_t g = 0; g < n_groups; g++) {
+            std::vector<int> idx(n_ranks);
+            for (int q = 0; q < n_ranks; q++) idx[q] = q;
+            auto a_of = [&](int q) { return r_lo[g * n_ranks + q] == 0 ? 0ull : bits_of(v_lo[g * n_ranks + q]); };
+            auto b_of = [&](int q) {
+                return r_hi[g * n_ranks + q] == NS - 1 ? 0x7fffffffffffffffull : bits_of(v_hi[g * n_ranks + q]);
+            };
+            std::sort(idx.begin(), idx.end(), [&](int x, int y) { return a_of(x) < a_of(y); });
+            for (int q : idx) {
+                const uint64_t a = a_of(q), b = b_of(q);
+                int l = nlist[g] - 1;
+                if (l >= 0 && a <= hi[g * MAX_LISTS + l]) {
+                    hi[g * MAX_LISTS + l] = std::max(hi[g * MAX_LISTS + l], b);
+                } else {
+                    l = nlist[g]++;
+                    lo[g * MAX_LISTS + l] = a;
+                    hi[g * MAX_LISTS + l] = b;
+                }
+                list_of[g * n_ranks + q] = l;
+                est[g * MAX_LISTS + l] += r_hi[g * n_ranks + q] - r_lo[g * n_ranks + q] + 1;
+            }
+        }
+        std::vector<int64_t> off(L6, 0), cap(L6, 0);
+        int64_t total = 0;
+        for (int64_t g = 0; g < n_groups; g++)
+            for (int l = 0; l < nlist[g]; l++) {
+                const double scale = (double)N / (double)NS;
+                const int64_t c = std::min<int64_t>(N, (int64_t)(4.0 * est[g * MAX_LISTS + l] * scale) + 4096);
+                off[g * MAX_LISTS + l] = total;
+                cap[g * MAX_LISTS + l] = c;
+                total += c;
+            }
+        // ---- 2. the one full pass: leaf sums + bracket counts/compaction ----
+        DBuf b_nl, b_lo, b_hi, b_off, b_cap, b_fill, b_below, b_cand;
+        if ((rc = b_nl.alloc(sizeof(int32_t) * n_groups, st)) || (rc = b_lo.alloc(8 * L6, st)) ||
+            (rc = b_hi.alloc(8 * L6, st)) || (rc = b_off.alloc(8 * L6, st)) || (rc = b_cap.alloc(8 * L6, st)) ||
+            (rc = b_fill.alloc(8 * L6, st)) || (rc = b_below.alloc(8 * L6, st)) ||
+            (rc = b_cand.alloc(sizeof(double) * std::max<int64_t>(total, 1), st)))
+            return rc;
+        cudaMemcpyAsync(b_nl.p, nlist.data(), b_nl.n, cudaMemcpyHostToDevice, st);
+        cudaMemcpyAsync(b_lo.p, lo.data(), b_lo.n, cudaMemcpyHostToDevice, st);
+        cudaMemcpyAsync(b_hi.p, hi.data(), b_hi.n, cudaMemcpyHostToDevice, st);
+        cudaMemcpyAsync(b_off.p, off.data(), b_off.n, cudaMemcpyHostToDevice, st);
+        cudaMemcpyAsync(b_cap.p, cap.data(), b_cap.n, cudaMemcpyHostToDevice, st);
+        cudaMemsetAsync(b_fill.p, 0, b_fill.n, st);
+        cudaMemsetAsync(b_below.p, 0, b_below.n, st);
+        if ((rc = leaf_pass(1, b_nl.as<int32_t>(), b_lo.as<uint64_t>(), b_hi.as<uint64_t>(), b_off.as<int64_t>(),
+                            b_cap.as<int64_t>(), b_fill.as<unsigned long long>(),
+                            b_below.as<unsigned long long>(), b_cand.as<double>())))
+            return rc;
+        if (!combined) {
+            if ((rc = combine())) return rc;
+            combined = true;
+        }
+        std::vector<unsigned long long> fill(L6), below(L6);
+        cudaMemcpyAsync(fill.data(), b_fill.p, b_fill.n, cudaMemcpyDeviceToHost, st);
+        cudaMemcpyAsync(below.data(), b_below.p, b_below.n, cudaMemcpyDeviceToHost, st);
+        if ((rc = check_cuda(cudaStreamSynchronize(st), "bracket sync"))) return rc;
+        // ---- 3. verify the brackets, exact rounds over the candidates ----
+        bool ok = true;
+        std::vector<SelSlot> slots(T);
+        for (size_t i = 0; i < T && ok; i++) {
+            const int64_t g = (int64_t)i / n_ranks;
+            const size_t li = g * MAX_LISTS + list_of[i];
+            const int64_t k = target[i];
+            if ((int64_t)fill[li] > cap[li] || (int64_t)below[li] > k || k >= (int64_t)(below[li] + fill[li])) {
+                ok = false;
+                break;
+            }
+            slots[i].prefix = 0;
+            slots[i].rank = k - (int64_t)below[li];
+            slots[i].cand_off = off[li];
+            slots[i].cand_len = (int64_t)fill[li];
+        }
+        if (!ok) continue;  // the sample missed a target (or overflowed): widen, retry
+        if ((rc = run_rounds(slots, b_cand.as<double>(), 48, st))) return rc;  // bits 63..0
+        for (size_t i = 0; i < T; i++) memcpy(&out_values[i], &slots[i].prefix, 8);
+        return CS_OK;
+    }
+    std::vector<double> vals;  // last resort: exact selection over everything
+    if ((rc = select_rows(d_resp, n_groups, rows_per_group, m, ldr, target, n_ranks, vals, st))) return rc;
+    for (size_t i = 0; i < vals.size(); i++) out_values[i] = vals[i];
+    return CS_OK;
 }

@@ -31,7 +31,9 @@ class SweepEngine:
     """P sweep points x R replications of n jobs, seed `seed`, reps
     [rep_begin, rep_begin + R) (a shard of n_reps_total when sharded)."""
 
-    KERNELS_PER_STEP = 1 + 1 + 2 + 1 + 3 * 2  # streams, sim, leaf+tree, compact, 3 digit rounds
+    # streams, sim; stats: 2 sample selections (hist0, compact, 3x2 digit rounds),
+    # leaf-sum+bracket pass, tree combine, 4x2 digit rounds on the candidates
+    KERNELS_PER_STEP = 1 + 1 + 2 * (1 + 1 + 6) + 1 + 1 + 8
 
     def __init__(self, rates_list: Sequence[Sequence[float]], caps_list: Sequence[Sequence[int]],
                  lams: Sequence[float], n_jobs: int, warmup_fraction: float, seed: int, reps: int,

@@ -228,3 +228,24 @@ def test_no_silent_fallback_loaded_native(eng):
     import paper_2604_14993_b200._native as N
 
     assert N._lib is not None and N.LIB_PATH.endswith("libchainserve_b200.so")
+
+
+def test_sample_select_and_fused_pairwise_means(eng, oracle):
+    """Groups above 2^20 responses take the sample-select path; per-rep means
+    come from the simulator's streamed numpy pairwise sum (bit-exact)."""
+    service, servers, _ = eng.petals_instance(10, 0.2, 101)
+    system = eng.greedy_cache_allocation(
+        eng.greedy_block_placement(servers, service, 7, 0.2, 0.7).placement)
+    nu = system.total_rate
+    lams = [0.3 * nu, 0.93 * nu]
+    n, wf, seed, R = 10_000, 0.1, 3, 128
+    res = eng.simulate_sweep([system.rates] * 2, [system.capacities] * 2, lams, n, wf, seed, R)
+    for p in range(2):
+        resp, busy, summ = oracle.simulate_reps(system.rates, system.capacities, lams[p], n, wf,
+                                                seed, 0, R, threads=8)
+        assert resp.size > (1 << 20)
+        merged = np.sort(resp.ravel())
+        for rank, v in res.order_stats[p].items():
+            assert same_float(v, merged[rank]), (p, rank, v, merged[rank])
+        means = np.array([row.mean() for row in resp])
+        assert np.array_equal(bits(res.summaries[p]["resp_mean"]), bits(means))
