@@ -241,6 +241,7 @@ def main():
         step()
     barrier()
     stage = []
+    launches0 = eng.lib.cs_launch_count()
     with ClockSampler(local) as clk:
         t_start = torch.cuda.Event(enable_timing=True)
         t_end = torch.cuda.Event(enable_timing=True)
@@ -251,6 +252,7 @@ def main():
         t_end.record()
         barrier()
     ms = t_start.elapsed_time(t_end)
+    launches = eng.lib.cs_launch_count() - launches0
     ms_t = torch.tensor([ms], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
@@ -312,7 +314,7 @@ def main():
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "jobs/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
-            "gpu_launches": SweepEngine.KERNELS_PER_STEP * args.steps,
+            "gpu_launches": int(launches),
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)

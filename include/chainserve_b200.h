@@ -44,6 +44,8 @@ const char* cs_last_error(void);
 int cs_host_log1p_variant(void);
 /* number of visible CUDA devices (0 when none) */
 int cs_device_count(void);
+/* kernels launched by this library since load (all threads) */
+int64_t cs_launch_count(void);
 
 /* ------------------------------------------------------------------------ */
 /* RNG                                                                        */

@@ -51,7 +51,7 @@ SUMMARY_DTYPE = np.dtype([(name, np.float64 if ct is C.c_double else np.int64)
 assert SUMMARY_DTYPE.itemsize == C.sizeof(RepSummary)
 
 EXPORTS = (
-    "cs_version", "cs_last_error", "cs_host_log1p_variant", "cs_device_count",
+    "cs_version", "cs_last_error", "cs_host_log1p_variant", "cs_device_count", "cs_launch_count",
     "cs_philox_keys", "cs_exp_streams", "cs_jffc_sim", "cs_jffc_sim_workspace_bytes",
     "cs_rep_stats", "cs_run_sim_host", "cs_gbp_batch", "cs_gca_batch",
 )
@@ -74,6 +74,7 @@ def load(require_device: bool = True):
         vp = C.c_void_p
         L.cs_version.restype = C.c_char_p
         L.cs_last_error.restype = C.c_char_p
+        L.cs_launch_count.restype = C.c_int64
         L.cs_philox_keys.argtypes = [P(C.c_uint32), C.c_int32, P(C.c_uint64), C.c_int64, P(C.c_uint64)]
         L.cs_exp_streams.argtypes = [vp, C.c_int64, C.c_int64, vp, C.c_int64, C.c_int32, vp]
         L.cs_jffc_sim.argtypes = [vp, C.c_int32, vp, vp, C.c_int32, C.c_int32, vp, C.c_int64,

@@ -5,6 +5,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <atomic>
 #include <vector>
 
 #include "cs_internal.cuh"
@@ -36,6 +37,9 @@ void set_error(const char* fmt, ...) {
     vsnprintf(g_err, sizeof(g_err), fmt, ap);
     va_end(ap);
 }
+
+static std::atomic<long long> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 void ensure_mem_pool() {
     static thread_local int done_dev = -1;
@@ -97,6 +101,7 @@ using namespace cs;
 extern "C" {
 
 const char* cs_version(void) { return "chainserve_b200 0.1.0 (sm_100a)"; }
+int64_t cs_launch_count(void) { return g_launches.load(); }
 const char* cs_last_error(void) { return g_err; }
 
 int cs_host_log1p_variant(void) {

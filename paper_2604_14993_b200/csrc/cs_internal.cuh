@@ -10,7 +10,12 @@ namespace cs {
 // Thread-local last-error message (cs_last_error()).
 void set_error(const char* fmt, ...);
 
+// Every kernel launch of the library is followed by check_launch(), which
+// also counts it (cs_launch_count(): evidence of the GPU path in benchmarks).
+void count_launch();
+
 inline int check_launch(const char* what) {
+    count_launch();
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
         set_error("%s: %s", what, cudaGetErrorString(e));

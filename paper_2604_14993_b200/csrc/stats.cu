@@ -1,28 +1,28 @@
-// stats.cu -- exact order statistics of the merged responses of each sweep
-// point: the values np.quantile interpolates between (sim.py:406,436-438).
+// stats.cu -- run_sim aggregation over the stored responses (sim.py:406-438).
 //
 // Per replication, responses.mean() (sim.py:407) is numpy's pairwise sum
 // (loops_utils.h.src @TYPE@_pairwise_sum: blocks <= 128 summed with 8
 // accumulators, larger ranges split at n/2 rounded down to a multiple of 8)
-// over the completion-ordered responses / count.  The split tree depends only
-// on the row length m; the host builds it once (leaves + post-order internal
-// nodes) and the device evaluates it bit-exactly: 8 lanes per leaf (lane j =
-// accumulator j), the exact ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) shuffle
-// combine, then a per-row walk of the internal nodes.
+// over the completion-ordered responses, divided by the count.  The split
+// tree depends only on the row length m; the host builds it once (leaves +
+// post-order internal nodes) and the device evaluates it bit-exactly: 8 lanes
+// per leaf (lane j = accumulator j), the exact ((r0+r1)+(r2+r3))+((r4+r5)+
+// (r6+r7)) shuffle combine, then a per-row walk of the internal nodes.
 //
-// Quantiles: an exact "sample-select" whose only full read of the responses
-// is fused with the leaf sums above:
-//   1. sample = the first ceil(m/32) responses of every row (contiguous, so
-//      1/32 of the bytes).  Exact order statistics of the sample at ranks
-//      k*|S|/N -+ delta (delta ~ 5 sigma) by MSB radix select on the IEEE bit
-//      patterns (responses are >= +0, so bit order == value order): a 15-bit
-//      digit-0 histogram, compaction of the selected buckets, three 16-bit
-//      digit rounds.  They bracket each target rank: [lo, hi].
-//   2. one coalesced pass over all responses counts, per target, the values
-//      below lo and compacts the values in [lo, hi] (warp-aggregated).
-//   3. if below <= k < below + |candidates| (checked; otherwise the bracket
-//      is widened and step 2 repeats), the k-th value is the (k - below)-th
-//      candidate: four 16-bit digit rounds over the candidates.
+// Quantiles need exact order statistics of each sweep point's merged
+// responses (the values np.quantile interpolates between).  An exact
+// sample-select whose only full read of the responses is the leaf-sum pass:
+//   1. sample = chunks of 32 consecutive responses every 1024 of each row
+//      (1/32 of the bytes, spread over the whole run).  Exact sample order
+//      statistics at ranks k|S|/N -+ 5 sigma bracket each target: MSB radix
+//      select on the IEEE bit patterns (responses >= +0, so bit order ==
+//      value order): 15-bit digit-0 histogram, compaction of the selected
+//      buckets, 12-bit digit rounds.
+//   2. the leaf-sum pass also counts the values below each bracket and
+//      compacts the values inside it (warp-aggregated appends).
+//   3. if below <= k < below + |inside| (verified; else the bracket widens and
+//      step 2 repeats), the k-th value is found by 12-bit digit rounds over
+//      the few candidates, starting below the bracket's common bit prefix.
 #include <cuda_runtime.h>
 #include <math.h>
 #include <string.h>
@@ -36,7 +36,8 @@ namespace cs {
 
 constexpr int H0_BITS = 15;
 constexpr int H0_BINS = 1 << H0_BITS;
-constexpr int HR_BINS = 1 << 16;
+constexpr int RD_BITS = 12;  // digit width of the selection rounds
+constexpr int RD_BINS = 1 << RD_BITS;
 constexpr int MAX_LISTS = 6;
 
 __device__ __forceinline__ uint64_t dbits(double v) { return (uint64_t)__double_as_longlong(v); }
@@ -52,11 +53,18 @@ int sm_count() {
     return n;
 }
 
-// Digit-0 (bits 62..48) histogram of the first `len` values of every row; a
-// block takes a contiguous range of rows and flushes its shared histogram
-// whenever the group changes.
+// Logical view of each row: logical index s -> physical (s / chunk) * stride + s % chunk.
+struct RowView {
+    int64_t len;     // logical values per row
+    int64_t chunk;   // consecutive values taken ...
+    int64_t stride;  // ... every `stride` values
+    __host__ __device__ int64_t phys(int64_t s) const { return (s / chunk) * stride + s % chunk; }
+};
+
+// Digit-0 (bits 62..48) histogram; a block takes a contiguous range of rows and
+// flushes its shared histogram whenever the group changes.
 __global__ void __launch_bounds__(1024) hist0_rows_kernel(const double* __restrict__ resp, int64_t n_rows,
-                                                          int64_t len, int64_t ldr, int64_t rows_per_group,
+                                                          RowView rv, int64_t ldr, int64_t rows_per_group,
                                                           uint32_t* __restrict__ hist0,
                                                           unsigned long long* __restrict__ n_bad) {
     extern __shared__ uint32_t sh[];
@@ -70,8 +78,8 @@ __global__ void __launch_bounds__(1024) hist0_rows_kernel(const double* __restri
         const int64_t ga = max(r0, g * rows_per_group), gb = min(r1, (g + 1) * rows_per_group);
         for (int64_t row = ga; row < gb; row++) {
             const double* __restrict__ a = resp + row * ldr;
-            for (int64_t q = threadIdx.x; q < len; q += blockDim.x) {
-                const uint64_t u = dbits(a[q]);
+            for (int64_t s = threadIdx.x; s < rv.len; s += blockDim.x) {
+                const uint64_t u = dbits(a[rv.phys(s)]);
                 if (u >> 63)
                     atomicAdd(n_bad, 1ull);
                 else
@@ -86,7 +94,7 @@ __global__ void __launch_bounds__(1024) hist0_rows_kernel(const double* __restri
     }
 }
 
-// Warp-aggregated append of v to list `list` (all lanes of the warp call it).
+// Warp-aggregated append of v to candidate list `list` (every lane calls it).
 __device__ __forceinline__ void append(int list, double v, unsigned long long* __restrict__ fill,
                                        const int64_t* __restrict__ off, const int64_t* __restrict__ cap,
                                        double* __restrict__ cand) {
@@ -104,9 +112,8 @@ __device__ __forceinline__ void append(int list, double v, unsigned long long* _
     }
 }
 
-// Sample compaction: values among the first `len` of each row whose digit 0
-// is one of the group's selected buckets.
-__global__ void compact_bucket_kernel(const double* __restrict__ resp, int64_t n_rows, int64_t len,
+// Compaction of the values whose digit 0 is one of the group's selected buckets.
+__global__ void compact_bucket_kernel(const double* __restrict__ resp, int64_t n_rows, RowView rv,
                                       int64_t ldr, int64_t rows_per_group,
                                       const int32_t* __restrict__ grp_nlist,
                                       const uint32_t* __restrict__ grp_bucket,
@@ -119,12 +126,12 @@ __global__ void compact_bucket_kernel(const double* __restrict__ resp, int64_t n
 #pragma unroll
         for (int q = 0; q < MAX_LISTS; q++) bk[q] = q < nl ? grp_bucket[g * MAX_LISTS + q] : 0xffffffffu;
         const double* __restrict__ a = resp + row * ldr;
-        for (int64_t base = 0; base < len; base += blockDim.x) {
-            const int64_t q0 = base + threadIdx.x;
+        for (int64_t base = 0; base < rv.len; base += blockDim.x) {
+            const int64_t s = base + threadIdx.x;
             int list = -1;
             double v = 0.0;
-            if (q0 < len) {
-                v = a[q0];
+            if (s < rv.len) {
+                v = a[rv.phys(s)];
                 const uint32_t d0 = (uint32_t)(dbits(v) >> 48);
 #pragma unroll
                 for (int q = 0; q < MAX_LISTS; q++)
@@ -135,8 +142,20 @@ __global__ void compact_bucket_kernel(const double* __restrict__ resp, int64_t n
     }
 }
 
-// Leaf sums (numpy pairwise leaves) + bracket counting/compaction, one pass.
-// blockIdx.y = group; warps take 4 leaves at a time (8 lanes per leaf).
+__device__ __forceinline__ int bracket_of(uint64_t w, const uint64_t* bl, const uint64_t* bh, uint32_t* cnt,
+                                          int64_t g) {
+    int list = -1;
+#pragma unroll
+    for (int q = 0; q < MAX_LISTS; q++) {
+        cnt[q] += w < bl[q];
+        if (w >= bl[q] && w <= bh[q]) list = (int)(g * MAX_LISTS + q);
+    }
+    return list;
+}
+
+// The one full pass: numpy pairwise leaf sums (8 lanes per leaf, 4 leaves per
+// warp; every value of a leaf is loaded up front for memory-level
+// parallelism) + optional bracket counting/compaction.  blockIdx.y = group.
 __global__ void __launch_bounds__(256) leaf_bracket_kernel(
     const double* __restrict__ resp, int64_t rows_per_group, int64_t ldr,
     const int32_t* __restrict__ leaf_off, const int32_t* __restrict__ leaf_len, int32_t L,
@@ -146,7 +165,7 @@ __global__ void __launch_bounds__(256) leaf_bracket_kernel(
     unsigned long long* __restrict__ below, double* __restrict__ cand) {
     const int64_t g = blockIdx.y;
     const int lane = threadIdx.x & 31, j = lane & 7, sub = lane >> 3;
-    const int64_t U = rows_per_group * (int64_t)L;  // leaves in this group
+    const int64_t U = rows_per_group * (int64_t)L;
     const int64_t warp_id = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int64_t n_warps = (int64_t)gridDim.x * (blockDim.x >> 5);
     const int nl = do_bracket ? grp_nlist[g] : 0;
@@ -165,52 +184,37 @@ __global__ void __launch_bounds__(256) leaf_bracket_kernel(
         const double* __restrict__ a = resp + row * ldr + (valid ? leaf_off[leaf] : 0);
         const int len = valid ? leaf_len[leaf] : 0;
         const int main_end = len >= 8 ? len - len % 8 : 0;
-        const int steps = __reduce_max_sync(0xffffffffu, (main_end + 7) >> 3);
-        double acc = 0.0;
-        for (int t = 0; t < steps; t++) {
-            const int idx = j + 8 * t;
-            const bool have = idx < main_end;
-            const double v = have ? a[idx] : 0.0;
-            acc = t == 0 ? v : (have ? __dadd_rn(acc, v) : acc);
-            if (do_bracket) {
-                int list = -1;
-                if (have) {
-                    const uint64_t w = dbits(v);
+        // accumulator j covers a[j], a[j+8], ... < main_end (<= 16 values)
+        double v[16];
 #pragma unroll
-                    for (int q = 0; q < MAX_LISTS; q++) {
-                        cnt[q] += w < bl[q];
-                        if (w >= bl[q] && w <= bh[q]) list = (int)(g * MAX_LISTS + q);
-                    }
-                }
-                append(list, v, fill, off, cap, cand);
+        for (int t = 0; t < 16; t++) v[t] = (j + 8 * t < main_end) ? a[j + 8 * t] : 0.0;
+        double acc = v[0];
+#pragma unroll
+        for (int t = 1; t < 16; t++)
+            if (j + 8 * t < main_end) acc = __dadd_rn(acc, v[t]);
+        if (do_bracket) {
+#pragma unroll
+            for (int t = 0; t < 16; t++) {
+                const bool have = j + 8 * t < main_end;
+                const int list = have ? bracket_of(dbits(v[t]), bl, bh, cnt, g) : -1;
+                append(list, v[t], fill, off, cap, cand);
             }
         }
         // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) in numpy's order
-        double s1 = __dadd_rn(acc, __shfl_down_sync(0xffffffffu, acc, 1));
-        double s2 = __dadd_rn(s1, __shfl_down_sync(0xffffffffu, s1, 2));
+        const double s1 = __dadd_rn(acc, __shfl_down_sync(0xffffffffu, acc, 1));
+        const double s2 = __dadd_rn(s1, __shfl_down_sync(0xffffffffu, s1, 2));
         double res = __dadd_rn(s2, __shfl_down_sync(0xffffffffu, s2, 4));
-        // remainder (only the last leaf of a row) / tiny leaves (< 8 values):
-        // lane j == 0 adds them sequentially; every lane joins the warp-wide append
+        // the remainder (last leaf of a row) or a tiny leaf (< 8 values): added
+        // sequentially by lane j == 0; all lanes join the warp-wide appends
         const int rem_begin = len >= 8 ? main_end : 0;
         if (len < 8) res = 0.0;
         const int rem = __reduce_max_sync(0xffffffffu, len - rem_begin);
         for (int t = 0; t < rem; t++) {
             const int idx = rem_begin + t;
             const bool have = j == 0 && idx < len;
-            const double v = have ? a[idx] : 0.0;
-            if (have) res = __dadd_rn(res, v);
-            if (do_bracket) {
-                int list = -1;
-                if (have) {
-                    const uint64_t w = dbits(v);
-#pragma unroll
-                    for (int q = 0; q < MAX_LISTS; q++) {
-                        cnt[q] += w < bl[q];
-                        if (w >= bl[q] && w <= bh[q]) list = (int)(g * MAX_LISTS + q);
-                    }
-                }
-                append(list, v, fill, off, cap, cand);
-            }
+            const double w = have ? a[idx] : 0.0;
+            if (have) res = __dadd_rn(res, w);
+            if (do_bracket) append(have ? bracket_of(dbits(w), bl, bh, cnt, g) : -1, w, fill, off, cap, cand);
         }
         if (valid && j == 0) leaf_sums[(g * rows_per_group) * (int64_t)L + u] = res;
     }
@@ -249,38 +253,46 @@ __global__ void tree_combine_kernel(const double* __restrict__ leaf_sums, int32_
 }
 
 struct SelSlot {
-    uint64_t prefix;   // selected high bits so far
+    uint64_t prefix;   // fixed high bits (above the current digit)
     int64_t rank;      // remaining rank among the candidates sharing the prefix
     int64_t cand_off;  // candidate list
     int64_t cand_len;
 };
 
-__global__ void round_hist_kernel(const double* __restrict__ cand, const SelSlot* __restrict__ slots,
-                                  int n_slots, int shift, uint32_t* __restrict__ hist) {
+// Histogram of the digit [shift, shift+12) over each slot's candidates that
+// match its prefix; shared-memory privatised (candidates cluster in few bins).
+__global__ void __launch_bounds__(512) round_hist_kernel(const double* __restrict__ cand,
+                                                         const SelSlot* __restrict__ slots, int n_slots,
+                                                         int shift, uint32_t* __restrict__ hist) {
+    __shared__ uint32_t sh[RD_BINS];
     const int s = blockIdx.y;
-    if (s >= n_slots) return;
     const SelSlot sl = slots[s];
-    const uint64_t hi_mask = shift + 16 >= 64 ? 0ull : ~((1ull << (shift + 16)) - 1);
-    uint32_t* h = hist + (int64_t)s * HR_BINS;
+    for (int b = threadIdx.x; b < RD_BINS; b += blockDim.x) sh[b] = 0;
+    __syncthreads();
+    const uint64_t hi_mask = shift + RD_BITS >= 64 ? 0ull : ~((1ull << (shift + RD_BITS)) - 1);
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < sl.cand_len;
          i += (int64_t)gridDim.x * blockDim.x) {
         const uint64_t u = dbits(cand[sl.cand_off + i]);
-        if ((u & hi_mask) == sl.prefix) atomicAdd(&h[(u >> shift) & 0xFFFF], 1u);
+        if ((u & hi_mask) == sl.prefix) atomicAdd(&sh[(u >> shift) & (RD_BINS - 1)], 1u);
     }
+    __syncthreads();
+    uint32_t* h = hist + (int64_t)s * RD_BINS;
+    for (int b = threadIdx.x; b < RD_BINS; b += blockDim.x)
+        if (sh[b]) atomicAdd(&h[b], sh[b]);
 }
 
-__global__ void __launch_bounds__(1024) round_select_kernel(SelSlot* __restrict__ slots, int n_slots,
-                                                            int shift, const uint32_t* __restrict__ hist) {
+__global__ void __launch_bounds__(1024) round_select_kernel(SelSlot* __restrict__ slots, int shift,
+                                                            const uint32_t* __restrict__ hist) {
     const int s = blockIdx.x;
-    if (s >= n_slots) return;
     __shared__ unsigned long long part[1024];
-    const uint32_t* h = hist + (int64_t)s * HR_BINS;
-    const int per = HR_BINS / blockDim.x;
+    const uint32_t* h = hist + (int64_t)s * RD_BINS;
+    constexpr int PER = RD_BINS / 1024;
     unsigned long long acc = 0;
-    for (int b = threadIdx.x * per; b < (threadIdx.x + 1) * per; b++) acc += h[b];
+#pragma unroll
+    for (int b = 0; b < PER; b++) acc += h[threadIdx.x * PER + b];
     part[threadIdx.x] = acc;
     __syncthreads();
-    for (int d = 1; d < (int)blockDim.x; d <<= 1) {
+    for (int d = 1; d < 1024; d <<= 1) {
         unsigned long long v = threadIdx.x >= (unsigned)d ? part[threadIdx.x - d] : 0ull;
         __syncthreads();
         part[threadIdx.x] += v;
@@ -290,7 +302,7 @@ __global__ void __launch_bounds__(1024) round_select_kernel(SelSlot* __restrict_
     const unsigned long long before = threadIdx.x ? part[threadIdx.x - 1] : 0ull;
     if ((long long)before <= rank && rank < (long long)part[threadIdx.x]) {
         unsigned long long c = before;
-        for (int b = threadIdx.x * per; b < (threadIdx.x + 1) * per; b++) {
+        for (int b = threadIdx.x * PER; b < (threadIdx.x + 1) * PER; b++) {
             if ((long long)(c + h[b]) > rank) {
                 slots[s].prefix |= ((uint64_t)b << shift);
                 slots[s].rank = rank - (long long)c;
@@ -328,34 +340,35 @@ static uint64_t bits_of(double d) {
     return u;
 }
 
-// Exact values for `slots` (prefix/rank preset) from candidate lists: 16-bit
-// digit rounds from bit `first_shift` down to 0.
+// 12-bit digit rounds at shifts first_shift, first_shift-12, ..., 0 (first_shift
+// a multiple of 12); slot prefixes must already hold the bits above first_shift+12.
 static int run_rounds(std::vector<SelSlot>& slots, const double* d_cand, int first_shift, cudaStream_t st) {
     const int n_slots = (int)slots.size();
     if (n_slots == 0) return CS_OK;
     DBuf b_slots, b_hist;
     int rc;
     if ((rc = b_slots.alloc(sizeof(SelSlot) * n_slots, st)) ||
-        (rc = b_hist.alloc(sizeof(uint32_t) * HR_BINS * (size_t)n_slots, st)))
+        (rc = b_hist.alloc(sizeof(uint32_t) * RD_BINS * (size_t)n_slots, st)))
         return rc;
     cudaMemcpyAsync(b_slots.p, slots.data(), b_slots.n, cudaMemcpyHostToDevice, st);
-    for (int shift = first_shift; shift >= 0; shift -= 16) {
+    int64_t max_len = 1;
+    for (auto& s : slots) max_len = std::max(max_len, s.cand_len);
+    const int bx = (int)std::max<int64_t>(1, std::min<int64_t>((max_len + 4095) / 4096, 64));
+    for (int shift = first_shift; shift >= 0; shift -= RD_BITS) {
         cudaMemsetAsync(b_hist.p, 0, b_hist.n, st);
-        dim3 grid(std::max(1, sm_count() * 4 / n_slots), n_slots);
-        round_hist_kernel<<<grid, 256, 0, st>>>(d_cand, b_slots.as<SelSlot>(), n_slots, shift,
-                                                b_hist.as<uint32_t>());
+        round_hist_kernel<<<dim3(bx, n_slots), 512, 0, st>>>(d_cand, b_slots.as<SelSlot>(), n_slots, shift,
+                                                              b_hist.as<uint32_t>());
         if ((rc = check_launch("round_hist_kernel"))) return rc;
-        round_select_kernel<<<n_slots, 1024, 0, st>>>(b_slots.as<SelSlot>(), n_slots, shift,
-                                                      b_hist.as<uint32_t>());
+        round_select_kernel<<<n_slots, 1024, 0, st>>>(b_slots.as<SelSlot>(), shift, b_hist.as<uint32_t>());
         if ((rc = check_launch("round_select_kernel"))) return rc;
     }
     cudaMemcpyAsync(slots.data(), b_slots.p, b_slots.n, cudaMemcpyDeviceToHost, st);
     return check_cuda(cudaStreamSynchronize(st), "rounds sync");
 }
 
-// Exact order statistics over the first `len` values of every row (groups of
+// Exact order statistics over the logical view of every row (groups of
 // rows_per_group rows); ranks: n_groups x n_ranks, 0-based.
-static int select_rows(const double* d_resp, int64_t n_groups, int64_t rows_per_group, int64_t len,
+static int select_rows(const double* d_resp, int64_t n_groups, int64_t rows_per_group, RowView rv,
                        int64_t ldr, const std::vector<int64_t>& ranks, int n_ranks, std::vector<double>& out,
                        cudaStream_t st) {
     const int64_t n_rows = n_groups * rows_per_group;
@@ -368,9 +381,9 @@ static int select_rows(const double* d_resp, int64_t n_groups, int64_t rows_per_
     cudaMemsetAsync(b_bad.p, 0, b_bad.n, st);
     const size_t smem = sizeof(uint32_t) * H0_BINS;
     cudaFuncSetAttribute(hist0_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    const int blocks = (int)std::min<int64_t>(n_rows, sm_count());
-    hist0_rows_kernel<<<blocks, 1024, smem, st>>>(d_resp, n_rows, len, ldr, rows_per_group,
-                                                  b_h0.as<uint32_t>(), b_bad.as<unsigned long long>());
+    const int blocks = (int)std::min<int64_t>(n_rows, 2 * sm_count());
+    hist0_rows_kernel<<<blocks, 1024, smem, st>>>(d_resp, n_rows, rv, ldr, rows_per_group, b_h0.as<uint32_t>(),
+                                                  b_bad.as<unsigned long long>());
     if ((rc = check_launch("hist0_rows_kernel"))) return rc;
     std::vector<uint32_t> h0((size_t)H0_BINS * n_groups);
     unsigned long long bad = 0;
@@ -427,10 +440,10 @@ static int select_rows(const double* d_resp, int64_t n_groups, int64_t rows_per_
     cudaMemcpyAsync(b_cap.p, cap.data(), b_cap.n, cudaMemcpyHostToDevice, st);
     cudaMemsetAsync(b_fill.p, 0, b_fill.n, st);
     compact_bucket_kernel<<<(unsigned)std::min<int64_t>(n_rows, (int64_t)sm_count() * 16), 256, 0, st>>>(
-        d_resp, n_rows, len, ldr, rows_per_group, b_nl.as<int32_t>(), b_bk.as<uint32_t>(),
-        b_off.as<int64_t>(), b_cap.as<int64_t>(), b_fill.as<unsigned long long>(), b_cand.as<double>());
+        d_resp, n_rows, rv, ldr, rows_per_group, b_nl.as<int32_t>(), b_bk.as<uint32_t>(), b_off.as<int64_t>(),
+        b_cap.as<int64_t>(), b_fill.as<unsigned long long>(), b_cand.as<double>());
     if ((rc = check_launch("compact_bucket_kernel"))) return rc;
-    if ((rc = run_rounds(slots, b_cand.as<double>(), 32, st))) return rc;  // bits 47..0
+    if ((rc = run_rounds(slots, b_cand.as<double>(), 36, st))) return rc;  // bits 47..0
     out.resize(slots.size());
     for (size_t i = 0; i < slots.size(); i++) memcpy(&out[i], &slots[i].prefix, 8);
     return CS_OK;
@@ -507,25 +520,25 @@ extern "C" int cs_rep_stats_impl(const double* d_resp, int32_t n_groups, int64_t
         (rc = b_ls.alloc(sizeof(double) * (size_t)n_rows * L, st)) ||
         (rc = b_sc.alloc(sizeof(double) * (size_t)n_rows * std::max(NN, 1), st)))
         return rc;
-    int32_t* d_lo_off = b_plan.as<int32_t>();
-    int32_t* d_lo_len = d_lo_off + L;
-    int32_t* d_nl = d_lo_len + L;
+    int32_t* d_leaf_off = b_plan.as<int32_t>();
+    int32_t* d_leaf_len = d_leaf_off + L;
+    int32_t* d_nl = d_leaf_len + L;
     int32_t* d_nr = d_nl + NN + 1;
-    cudaMemcpyAsync(d_lo_off, pl.leaf_off.data(), sizeof(int32_t) * L, cudaMemcpyHostToDevice, st);
-    cudaMemcpyAsync(d_lo_len, pl.leaf_len.data(), sizeof(int32_t) * L, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(d_leaf_off, pl.leaf_off.data(), sizeof(int32_t) * L, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(d_leaf_len, pl.leaf_len.data(), sizeof(int32_t) * L, cudaMemcpyHostToDevice, st);
     if (NN) {
         cudaMemcpyAsync(d_nl, pl.node_l.data(), sizeof(int32_t) * NN, cudaMemcpyHostToDevice, st);
         cudaMemcpyAsync(d_nr, pl.node_r.data(), sizeof(int32_t) * NN, cudaMemcpyHostToDevice, st);
     }
     const int64_t U = rows_per_group * (int64_t)L;
-    const int bx = (int)std::max<int64_t>(1, std::min<int64_t>((U + 31) / 32, (int64_t)sm_count() * 8 / n_groups + 1));
+    const int bx = (int)std::max<int64_t>(
+        1, std::min<int64_t>((U + 31) / 32, ((int64_t)sm_count() * 8 + n_groups - 1) / n_groups));
     auto leaf_pass = [&](int do_bracket, const int32_t* nl, const uint64_t* lo, const uint64_t* hi,
                          const int64_t* off, const int64_t* cap, unsigned long long* fill,
                          unsigned long long* below, double* cand) {
-        dim3 grid(bx, n_groups);
-        leaf_bracket_kernel<<<grid, 256, 0, st>>>(d_resp, rows_per_group, ldr, d_lo_off, d_lo_len, L,
-                                                  b_ls.as<double>(), do_bracket, nl, lo, hi, off, cap, fill,
-                                                  below, cand);
+        leaf_bracket_kernel<<<dim3(bx, n_groups), 256, 0, st>>>(d_resp, rows_per_group, ldr, d_leaf_off,
+                                                                d_leaf_len, L, b_ls.as<double>(), do_bracket, nl,
+                                                                lo, hi, off, cap, fill, below, cand);
         return check_launch("leaf_bracket_kernel");
     };
     auto combine = [&]() {
@@ -533,18 +546,20 @@ extern "C" int cs_rep_stats_impl(const double* d_resp, int32_t n_groups, int64_t
             b_ls.as<double>(), L, d_nl, d_nr, NN, b_sc.as<double>(), n_rows, m, d_summ, d_row_sums);
         return check_launch("tree_combine_kernel");
     };
-    const int64_t ms = (m + 31) / 32;
-    if (!want_ranks || N <= (1 << 20) || ms < 8) {
+    const RowView full{m, m, m};
+    const int64_t n_chunks = m / 1024, tail = std::min<int64_t>(32, m % 1024);
+    const RowView sample{n_chunks * 32 + tail, 32, 1024};  // 32 of every 1024 responses
+    if (!want_ranks || N <= (1 << 20) || sample.len < 64) {
         if ((rc = leaf_pass(0, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr)) ||
             (rc = combine()))
             return rc;
         if (!want_ranks) return CS_OK;
         std::vector<double> vals;  // small groups: exact selection over all values
-        if ((rc = select_rows(d_resp, n_groups, rows_per_group, m, ldr, target, n_ranks, vals, st))) return rc;
+        if ((rc = select_rows(d_resp, n_groups, rows_per_group, full, ldr, target, n_ranks, vals, st))) return rc;
         for (size_t i = 0; i < vals.size(); i++) out_values[i] = vals[i];
         return CS_OK;
     }
-    const int64_t NS = rows_per_group * ms;  // sample size per group
+    const int64_t NS = rows_per_group * sample.len;  // sample size per group
     const size_t T = target.size();
     bool combined = false;
     double widen = 1.0;
@@ -559,8 +574,8 @@ extern "C" int cs_rep_stats_impl(const double* d_resp, int32_t n_groups, int64_t
             r_hi[i] = std::min<int64_t>(NS - 1, (int64_t)ceil(ks + delta));
         }
         std::vector<double> v_lo, v_hi;
-        if ((rc = select_rows(d_resp, n_groups, rows_per_group, ms, ldr, r_lo, n_ranks, v_lo, st)) ||
-            (rc = select_rows(d_resp, n_groups, rows_per_group, ms, ldr, r_hi, n_ranks, v_hi, st)))
+        if ((rc = select_rows(d_resp, n_groups, rows_per_group, sample, ldr, r_lo, n_ranks, v_lo, st)) ||
+            (rc = select_rows(d_resp, n_groups, rows_per_group, sample, ldr, r_hi, n_ranks, v_hi, st)))
             return rc;
         std::vector<int32_t> nlist(n_groups, 0);
         const size_t L6 = (size_t)n_groups * MAX_LISTS;
@@ -591,6 +606,7 @@ extern "C" int cs_rep_stats_impl(const double* d_resp, int32_t n_groups, int64_t
         }
         std::vector<int64_t> off(L6, 0), cap(L6, 0);
         int64_t total = 0;
+        int top_bit = 0;  // highest bit where some bracket's lo and hi differ
         for (int64_t g = 0; g < n_groups; g++)
             for (int l = 0; l < nlist[g]; l++) {
                 const double scale = (double)N / (double)NS;
@@ -598,6 +614,8 @@ extern "C" int cs_rep_stats_impl(const double* d_resp, int32_t n_groups, int64_t
                 off[g * MAX_LISTS + l] = total;
                 cap[g * MAX_LISTS + l] = c;
                 total += c;
+                const uint64_t d = lo[g * MAX_LISTS + l] ^ hi[g * MAX_LISTS + l];
+                if (d) top_bit = std::max(top_bit, 63 - __builtin_clzll(d));
             }
         // ---- 2. the one full pass: leaf sums + bracket counts/compaction ----
         DBuf b_nl, b_lo, b_hi, b_off, b_cap, b_fill, b_below, b_cand;
@@ -614,8 +632,8 @@ extern "C" int cs_rep_stats_impl(const double* d_resp, int32_t n_groups, int64_t
         cudaMemsetAsync(b_fill.p, 0, b_fill.n, st);
         cudaMemsetAsync(b_below.p, 0, b_below.n, st);
         if ((rc = leaf_pass(1, b_nl.as<int32_t>(), b_lo.as<uint64_t>(), b_hi.as<uint64_t>(), b_off.as<int64_t>(),
-                            b_cap.as<int64_t>(), b_fill.as<unsigned long long>(),
-                            b_below.as<unsigned long long>(), b_cand.as<double>())))
+                            b_cap.as<int64_t>(), b_fill.as<unsigned long long>(), b_below.as<unsigned long long>(),
+                            b_cand.as<double>())))
             return rc;
         if (!combined) {
             if ((rc = combine())) return rc;
@@ -626,6 +644,8 @@ extern "C" int cs_rep_stats_impl(const double* d_resp, int32_t n_groups, int64_t
         cudaMemcpyAsync(below.data(), b_below.p, b_below.n, cudaMemcpyDeviceToHost, st);
         if ((rc = check_cuda(cudaStreamSynchronize(st), "bracket sync"))) return rc;
         // ---- 3. verify the brackets, exact rounds over the candidates ----
+        const int first_shift = (top_bit / RD_BITS) * RD_BITS;  // digits cover bits <= top_bit
+        const uint64_t keep = first_shift + RD_BITS >= 64 ? 0ull : ~((1ull << (first_shift + RD_BITS)) - 1);
         bool ok = true;
         std::vector<SelSlot> slots(T);
         for (size_t i = 0; i < T && ok; i++) {
@@ -636,18 +656,18 @@ extern "C" int cs_rep_stats_impl(const double* d_resp, int32_t n_groups, int64_t
                 ok = false;
                 break;
             }
-            slots[i].prefix = 0;
+            slots[i].prefix = lo[li] & keep;  // bits shared by every candidate of the bracket
             slots[i].rank = k - (int64_t)below[li];
             slots[i].cand_off = off[li];
             slots[i].cand_len = (int64_t)fill[li];
         }
         if (!ok) continue;  // the sample missed a target (or overflowed): widen, retry
-        if ((rc = run_rounds(slots, b_cand.as<double>(), 48, st))) return rc;  // bits 63..0
+        if ((rc = run_rounds(slots, b_cand.as<double>(), first_shift, st))) return rc;
         for (size_t i = 0; i < T; i++) memcpy(&out_values[i], &slots[i].prefix, 8);
         return CS_OK;
     }
     std::vector<double> vals;  // last resort: exact selection over everything
-    if ((rc = select_rows(d_resp, n_groups, rows_per_group, m, ldr, target, n_ranks, vals, st))) return rc;
+    if ((rc = select_rows(d_resp, n_groups, rows_per_group, full, ldr, target, n_ranks, vals, st))) return rc;
     for (size_t i = 0; i < vals.size(); i++) out_values[i] = vals[i];
     return CS_OK;
 }
