@@ -218,8 +218,12 @@ def main():
     rates, caps = compose_engine(service, servers)
     lams, nu = lam_grid(rates, caps, args.points)
     R = args.reps
+    if world > 1:
+        from paper_2604_14993_b200 import distributed as D
+
+        D.init()  # the engine's NCCL communicator (final statistics only)
     eng = SweepEngine([rates] * args.points, [caps] * args.points, lams, args.jobs, 0.1, 1, R,
-                      rep_begin=rank * R)
+                      rep_begin=rank * R, distributed=world > 1, total_reps=world * R)
     jobs_per_step = args.points * R * args.jobs
 
     def barrier():
@@ -277,12 +281,19 @@ def main():
     e2e_value = None
     h2d = args.points * 16 + len(rates) * 12 * args.points + 16 * R
     d2h = args.points * R * (128 + 8 * eng.ldb) + args.points * (1 << 15) * 4 + 6 * 8 * args.points
+    if world > 1:  # the sharded public API: world*R replications split over the ranks
+        cfgs = [P.SimConfig(rates=rates, capacities=caps, workload=P.PoissonWorkload(l),
+                            horizon_jobs=args.jobs, warmup_fraction=0.1, seed=1,
+                            replications=world * R) for l in lams]
+        run_api = D.run_sim_sharded
+    else:
+        run_api = P.run_sim_batch
     if args.e2e_steps > 0:
-        P.run_sim_batch(cfgs)  # warm the allocator pool
+        run_api(cfgs)  # warm the allocator pools
         barrier()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
-            stats = P.run_sim_batch(cfgs)
+            stats = run_api(cfgs)
         barrier()
         e2e_s = (time.perf_counter() - t0) / args.e2e_steps
         e2e_t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
@@ -304,7 +315,8 @@ def main():
                             f"{args.jobs} jobs per GPU",
                 "jobs_per_step": world * jobs_per_step,
                 "l2": "inputs larger than L2 (responses 8 B/job stored in HBM)",
-                "parallelism": f"replicas sharded over {world} GPU(s), NCCL all-gather of summaries",
+                "parallelism": f"replicas sharded over {world} GPU(s) ({R} per GPU); NCCL all-gather of "
+                           "summaries + all-reduced radix-select histograms for exact global quantiles",
             },
             "stages_ms": {"streams": streams_ms, "jffc_sim": sim_ms, "stats": stats_ms},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

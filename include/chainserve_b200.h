@@ -134,6 +134,25 @@ int cs_rep_stats(const double* d_resp, int32_t n_groups, int64_t rows_per_group,
                  int64_t ldr, cs_rep_summary* d_summary, const int64_t* ranks, int32_t n_ranks,
                  double* out_values, double* d_row_sums, void* stream);
 
+/* Sharded variant (one process per GPU, after cs_comm_init): every rank holds
+ * rows_per_group rows of each group (equal shards); ranks index the union of
+ * all ranks' responses; the histograms and bracket counts are all-reduced
+ * over NCCL so every rank returns the same exact global order statistics. */
+int cs_rep_stats_dist(const double* d_resp, int32_t n_groups, int64_t rows_per_group, int64_t m,
+                      int64_t ldr, cs_rep_summary* d_summary, const int64_t* ranks, int32_t n_ranks,
+                      double* out_values, double* d_row_sums, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* Multi-GPU: the engine's NCCL communicator (one process per GPU)            */
+/* ------------------------------------------------------------------------ */
+/* Replications shard across GPUs with no data-path exchange (sim.py:400-404
+ * replications are independent); the only collectives are the final
+ * statistics (cs_rep_stats_dist).  Rank 0 creates the id, the driver
+ * broadcasts it (torch.distributed), every rank calls cs_comm_init. */
+int cs_nccl_unique_id(void* out128);
+int cs_comm_init(const void* unique_id128, int32_t nranks, int32_t rank);
+int cs_comm_destroy(void);
+
 /* ------------------------------------------------------------------------ */
 /* End to end from HOST buffers                                               */
 /* ------------------------------------------------------------------------ */

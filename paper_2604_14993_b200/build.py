@@ -21,7 +21,19 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 BUILD = os.path.join(ROOT, "build", "csrc")
 LIB = os.path.join(PKG, "libchainserve_b200.so")
-SOURCES = ["capi.cu", "exp_stream.cu", "jffc_sim.cu", "stats.cu", "compose.cu"]
+SOURCES = ["capi.cu", "exp_stream.cu", "jffc_sim.cu", "stats.cu", "compose.cu", "dist.cu"]
+
+
+def nccl_dirs():
+    """NCCL 2.28 shipped with the torch wheels (nvidia-nccl-cu12)."""
+    import importlib.util
+
+    spec = importlib.util.find_spec("nvidia")
+    for base in (list(spec.submodule_search_locations) if spec else []):
+        inc, lib = os.path.join(base, "nccl", "include"), os.path.join(base, "nccl", "lib")
+        if os.path.exists(os.path.join(inc, "nccl.h")):
+            return inc, lib
+    raise RuntimeError("nccl.h not found (expected nvidia/nccl from the torch wheels)")
 
 
 def nvcc() -> str:
@@ -36,7 +48,7 @@ def flags(verbose: bool):
         "-gencode", "arch=compute_100a,code=sm_100a",
         "-O3", "-lineinfo", "-std=c++17", "-fmad=false",
         "-Xcompiler", "-fPIC,-ffp-contract=off,-O2",
-        "-I", os.path.join(ROOT, "include"), "-I", CSRC,
+        "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", nccl_dirs()[0],
     ]
     if verbose:
         f += ["-Xptxas", "-v"]
@@ -70,8 +82,9 @@ def build(verbose: bool = False, force: bool = False) -> str:
             if res.returncode:
                 raise RuntimeError(f"nvcc failed: {' '.join(cmd)}")
     if force or jobs or not os.path.exists(LIB):
+        nccl_lib = nccl_dirs()[1]
         link = [cc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB, *objs,
-                "-lcudart"]
+                "-lcudart", "-L", nccl_lib, "-l:libnccl.so.2", "-Xlinker", f"-rpath={nccl_lib}"]
         res = subprocess.run(link, capture_output=True, text=True)
         if res.returncode:
             sys.stderr.write(res.stdout + res.stderr)

@@ -18,7 +18,7 @@ extern "C" int cs_jffc_sim_impl(const cs_sim_point*, int32_t, const double*, con
                                 void*, int64_t, void*);
 extern "C" int64_t cs_jffc_sim_workspace_bytes_impl(int32_t, int32_t, int32_t, int32_t, int64_t);
 extern "C" int cs_rep_stats_impl(const double*, int32_t, int64_t, int64_t, int64_t, cs_rep_summary*,
-                                 const int64_t*, int32_t, double*, double*, void*);
+                                 const int64_t*, int32_t, double*, double*, int32_t, void*);
 extern "C" int cs_gbp_batch_impl(const cs_compose_point*, int32_t, int32_t, const int64_t*,
                                  const double*, const double*, const int32_t*, int32_t*, int32_t*,
                                  int32_t*, double*, int32_t*, int32_t*, int32_t*, double*, int32_t*,
@@ -190,7 +190,19 @@ int cs_rep_stats(const double* d_resp, int32_t n_groups, int64_t rows_per_group,
     }
     ensure_mem_pool();
     return cs_rep_stats_impl(d_resp, n_groups, rows_per_group, m, ldr, d_summary, ranks, n_ranks,
-                             out_values, d_row_sums, stream);
+                             out_values, d_row_sums, 0, stream);
+}
+
+int cs_rep_stats_dist(const double* d_resp, int32_t n_groups, int64_t rows_per_group, int64_t m,
+                      int64_t ldr, cs_rep_summary* d_summary, const int64_t* ranks, int32_t n_ranks,
+                      double* out_values, double* d_row_sums, void* stream) {
+    if (cs_device_count() == 0) {
+        set_error("cs_rep_stats_dist: no CUDA device");
+        return CS_ERR_CUDA;
+    }
+    ensure_mem_pool();
+    return cs_rep_stats_impl(d_resp, n_groups, rows_per_group, m, ldr, d_summary, ranks, n_ranks,
+                             out_values, d_row_sums, 1, stream);
 }
 
 int cs_gbp_batch(const cs_compose_point* d_points, int32_t n_points, int32_t max_servers,
@@ -312,7 +324,7 @@ int cs_run_sim_host(const cs_sim_point* points, int32_t n_points, const double* 
         if (c0 + chunk < n_reps && (rc = check_cuda(cudaStreamSynchronize(st), "chunk sync"))) return rc;
     }
     rc = cs_rep_stats_impl((const double*)b_resp.p, n_points, n_reps, m, ldr, (cs_rep_summary*)b_summ.p,
-                           ranks, n_ranks, out_rank_values, nullptr, st);
+                           ranks, n_ranks, out_rank_values, nullptr, 0, st);
     if (rc) return rc;
     cudaMemcpyAsync(out_summary, b_summ.p, sizeof(cs_rep_summary) * rows, cudaMemcpyDeviceToHost, st);
     if (out_busy) cudaMemcpyAsync(out_busy, b_busy.p, sizeof(double) * ldb * rows, cudaMemcpyDeviceToHost, st);

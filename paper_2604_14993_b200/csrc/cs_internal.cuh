@@ -36,6 +36,14 @@ inline int check_cuda(cudaError_t e, const char* what) {
 // returning them to the OS at every synchronisation (default threshold 0).
 void ensure_mem_pool();
 
+// NCCL all-reduces of the sharded statistics (dist.cu); no-ops without a
+// multi-rank communicator.
+bool dist_active();
+int dist_nranks();
+int allreduce_u32(void* buf, size_t count, cudaStream_t st);
+int allreduce_u64(void* buf, size_t count, cudaStream_t st);
+int allreduce_max_u64(void* buf, size_t count, cudaStream_t st);
+
 // Python-semantics helpers (no contraction; explicit IEEE round-to-nearest).
 __device__ __forceinline__ double py_div(double a, double b) { return __ddiv_rn(a, b); }
 

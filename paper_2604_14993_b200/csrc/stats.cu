@@ -56,9 +56,11 @@ int sm_count() {
 // Logical view of each row: logical index s -> physical (s / chunk) * stride + s % chunk.
 struct RowView {
     int64_t len;     // logical values per row
-    int64_t chunk;   // consecutive values taken ...
-    int64_t stride;  // ... every `stride` values
-    __host__ __device__ int64_t phys(int64_t s) const { return (s / chunk) * stride + s % chunk; }
+    int32_t chunk_log2;   // 2^chunk_log2 consecutive values taken ...
+    int32_t stride_log2;  // ... every 2^stride_log2 values (chunk == stride: contiguous)
+    __host__ __device__ int64_t phys(int64_t s) const {
+        return ((s >> chunk_log2) << stride_log2) | (s & ((1ll << chunk_log2) - 1));
+    }
 };
 
 // Digit-0 (bits 62..48) histogram; a block takes a contiguous range of rows and
@@ -179,8 +181,10 @@ __global__ void __launch_bounds__(256) leaf_bracket_kernel(
     for (int64_t base = warp_id * 4; base < U; base += n_warps * 4) {
         const int64_t u = base + sub;
         const bool valid = u < U;
-        const int64_t row = g * rows_per_group + (valid ? u / L : 0);
-        const int leaf = valid ? (int)(u % L) : 0;
+        // U < 2^31 is checked on the host: 32-bit division
+        const uint32_t uq = valid ? (uint32_t)u / (uint32_t)L : 0u;
+        const int64_t row = g * rows_per_group + uq;
+        const int leaf = valid ? (int)((uint32_t)u - uq * (uint32_t)L) : 0;
         const double* __restrict__ a = resp + row * ldr + (valid ? leaf_off[leaf] : 0);
         const int len = valid ? leaf_len[leaf] : 0;
         const int main_end = len >= 8 ? len - len % 8 : 0;
@@ -342,7 +346,8 @@ static uint64_t bits_of(double d) {
 
 // 12-bit digit rounds at shifts first_shift, first_shift-12, ..., 0 (first_shift
 // a multiple of 12); slot prefixes must already hold the bits above first_shift+12.
-static int run_rounds(std::vector<SelSlot>& slots, const double* d_cand, int first_shift, cudaStream_t st) {
+static int run_rounds(std::vector<SelSlot>& slots, const double* d_cand, int first_shift, bool dist,
+                      cudaStream_t st) {
     const int n_slots = (int)slots.size();
     if (n_slots == 0) return CS_OK;
     DBuf b_slots, b_hist;
@@ -359,6 +364,7 @@ static int run_rounds(std::vector<SelSlot>& slots, const double* d_cand, int fir
         round_hist_kernel<<<dim3(bx, n_slots), 512, 0, st>>>(d_cand, b_slots.as<SelSlot>(), n_slots, shift,
                                                               b_hist.as<uint32_t>());
         if ((rc = check_launch("round_hist_kernel"))) return rc;
+        if (dist && (rc = allreduce_u32(b_hist.p, (size_t)RD_BINS * n_slots, st))) return rc;
         round_select_kernel<<<n_slots, 1024, 0, st>>>(b_slots.as<SelSlot>(), shift, b_hist.as<uint32_t>());
         if ((rc = check_launch("round_select_kernel"))) return rc;
     }
@@ -370,7 +376,7 @@ static int run_rounds(std::vector<SelSlot>& slots, const double* d_cand, int fir
 // rows_per_group rows); ranks: n_groups x n_ranks, 0-based.
 static int select_rows(const double* d_resp, int64_t n_groups, int64_t rows_per_group, RowView rv,
                        int64_t ldr, const std::vector<int64_t>& ranks, int n_ranks, std::vector<double>& out,
-                       cudaStream_t st) {
+                       bool dist, cudaStream_t st) {
     const int64_t n_rows = n_groups * rows_per_group;
     int rc;
     DBuf b_h0, b_bad;
@@ -385,6 +391,9 @@ static int select_rows(const double* d_resp, int64_t n_groups, int64_t rows_per_
     hist0_rows_kernel<<<blocks, 1024, smem, st>>>(d_resp, n_rows, rv, ldr, rows_per_group, b_h0.as<uint32_t>(),
                                                   b_bad.as<unsigned long long>());
     if ((rc = check_launch("hist0_rows_kernel"))) return rc;
+    if (dist && ((rc = allreduce_u32(b_h0.p, (size_t)H0_BINS * n_groups, st)) ||
+                 (rc = allreduce_u64(b_bad.p, 1, st))))
+        return rc;
     std::vector<uint32_t> h0((size_t)H0_BINS * n_groups);
     unsigned long long bad = 0;
     cudaMemcpyAsync(h0.data(), b_h0.p, b_h0.n, cudaMemcpyDeviceToHost, st);
@@ -443,7 +452,7 @@ static int select_rows(const double* d_resp, int64_t n_groups, int64_t rows_per_
         d_resp, n_rows, rv, ldr, rows_per_group, b_nl.as<int32_t>(), b_bk.as<uint32_t>(), b_off.as<int64_t>(),
         b_cap.as<int64_t>(), b_fill.as<unsigned long long>(), b_cand.as<double>());
     if ((rc = check_launch("compact_bucket_kernel"))) return rc;
-    if ((rc = run_rounds(slots, b_cand.as<double>(), 36, st))) return rc;  // bits 47..0
+    if ((rc = run_rounds(slots, b_cand.as<double>(), 36, dist, st))) return rc;  // bits 47..0
     out.resize(slots.size());
     for (size_t i = 0; i < slots.size(); i++) memcpy(&out[i], &slots[i].prefix, 8);
     return CS_OK;
@@ -490,8 +499,13 @@ using namespace cs;
 
 extern "C" int cs_rep_stats_impl(const double* d_resp, int32_t n_groups, int64_t rows_per_group, int64_t m,
                                  int64_t ldr, cs_rep_summary* d_summ, const int64_t* ranks,
-                                 int32_t n_ranks, double* out_values, double* d_row_sums, void* stream) {
+                                 int32_t n_ranks, double* out_values, double* d_row_sums, int32_t dist_flag,
+                                 void* stream) {
     cudaStream_t st = (cudaStream_t)stream;
+    // sharded: every rank holds rows_per_group rows of each group (equal shards);
+    // ranks refer to the union over all ranks
+    const bool dist = dist_flag && dist_active();
+    const int64_t shards = dist ? dist_nranks() : 1;
     const int64_t n_rows = (int64_t)n_groups * rows_per_group;
     if (n_rows == 0 || m == 0) return CS_OK;
     if (ranks != nullptr && n_ranks > MAX_LISTS) {
@@ -499,7 +513,7 @@ extern "C" int cs_rep_stats_impl(const double* d_resp, int32_t n_groups, int64_t
         return CS_INVALID;
     }
     const bool want_ranks = ranks != nullptr && n_ranks > 0;
-    const int64_t N = rows_per_group * m;  // values per group
+    const int64_t N = rows_per_group * m * shards;  // values per group (all shards)
     std::vector<int64_t> target(want_ranks ? (size_t)n_groups * n_ranks : 0);
     for (size_t i = 0; i < target.size(); i++) {
         int64_t k = ranks[i];
@@ -531,6 +545,10 @@ extern "C" int cs_rep_stats_impl(const double* d_resp, int32_t n_groups, int64_t
         cudaMemcpyAsync(d_nr, pl.node_r.data(), sizeof(int32_t) * NN, cudaMemcpyHostToDevice, st);
     }
     const int64_t U = rows_per_group * (int64_t)L;
+    if (U >= (1ll << 31)) {
+        set_error("cs_rep_stats: more than 2^31 pairwise leaves per group");
+        return CS_UNSUPPORTED;
+    }
     const int bx = (int)std::max<int64_t>(
         1, std::min<int64_t>((U + 31) / 32, ((int64_t)sm_count() * 8 + n_groups - 1) / n_groups));
     auto leaf_pass = [&](int do_bracket, const int32_t* nl, const uint64_t* lo, const uint64_t* hi,
@@ -546,20 +564,21 @@ extern "C" int cs_rep_stats_impl(const double* d_resp, int32_t n_groups, int64_t
             b_ls.as<double>(), L, d_nl, d_nr, NN, b_sc.as<double>(), n_rows, m, d_summ, d_row_sums);
         return check_launch("tree_combine_kernel");
     };
-    const RowView full{m, m, m};
+    const RowView full{m, 40, 40};  // contiguous
     const int64_t n_chunks = m / 1024, tail = std::min<int64_t>(32, m % 1024);
-    const RowView sample{n_chunks * 32 + tail, 32, 1024};  // 32 of every 1024 responses
+    const RowView sample{n_chunks * 32 + tail, 5, 10};  // 32 of every 1024 responses
     if (!want_ranks || N <= (1 << 20) || sample.len < 64) {
         if ((rc = leaf_pass(0, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr)) ||
             (rc = combine()))
             return rc;
         if (!want_ranks) return CS_OK;
         std::vector<double> vals;  // small groups: exact selection over all values
-        if ((rc = select_rows(d_resp, n_groups, rows_per_group, full, ldr, target, n_ranks, vals, st))) return rc;
+        if ((rc = select_rows(d_resp, n_groups, rows_per_group, full, ldr, target, n_ranks, vals, dist, st)))
+            return rc;
         for (size_t i = 0; i < vals.size(); i++) out_values[i] = vals[i];
         return CS_OK;
     }
-    const int64_t NS = rows_per_group * sample.len;  // sample size per group
+    const int64_t NS = rows_per_group * sample.len * shards;  // sample size per group
     const size_t T = target.size();
     bool combined = false;
     double widen = 1.0;
@@ -574,8 +593,8 @@ extern "C" int cs_rep_stats_impl(const double* d_resp, int32_t n_groups, int64_t
             r_hi[i] = std::min<int64_t>(NS - 1, (int64_t)ceil(ks + delta));
         }
         std::vector<double> v_lo, v_hi;
-        if ((rc = select_rows(d_resp, n_groups, rows_per_group, sample, ldr, r_lo, n_ranks, v_lo, st)) ||
-            (rc = select_rows(d_resp, n_groups, rows_per_group, sample, ldr, r_hi, n_ranks, v_hi, st)))
+        if ((rc = select_rows(d_resp, n_groups, rows_per_group, sample, ldr, r_lo, n_ranks, v_lo, dist, st)) ||
+            (rc = select_rows(d_resp, n_groups, rows_per_group, sample, ldr, r_hi, n_ranks, v_hi, dist, st)))
             return rc;
         std::vector<int32_t> nlist(n_groups, 0);
         const size_t L6 = (size_t)n_groups * MAX_LISTS;
@@ -639,10 +658,22 @@ extern "C" int cs_rep_stats_impl(const double* d_resp, int32_t n_groups, int64_t
             if ((rc = combine())) return rc;
             combined = true;
         }
-        std::vector<unsigned long long> fill(L6), below(L6);
+        std::vector<unsigned long long> fill(L6), below(L6), fill_all(L6), overflow(L6);
         cudaMemcpyAsync(fill.data(), b_fill.p, b_fill.n, cudaMemcpyDeviceToHost, st);
-        cudaMemcpyAsync(below.data(), b_below.p, b_below.n, cudaMemcpyDeviceToHost, st);
         if ((rc = check_cuda(cudaStreamSynchronize(st), "bracket sync"))) return rc;
+        for (size_t li = 0; li < L6; li++) overflow[li] = (int64_t)fill[li] > cap[li] ? 1 : 0;
+        if (dist) {  // global below / inside counts and any-rank overflow
+            DBuf b_ov;
+            if ((rc = b_ov.alloc(8 * L6, st))) return rc;
+            cudaMemcpyAsync(b_ov.p, overflow.data(), 8 * L6, cudaMemcpyHostToDevice, st);
+            if ((rc = allreduce_u64(b_below.p, L6, st)) || (rc = allreduce_u64(b_fill.p, L6, st)) ||
+                (rc = allreduce_max_u64(b_ov.p, L6, st)))
+                return rc;
+            cudaMemcpyAsync(overflow.data(), b_ov.p, 8 * L6, cudaMemcpyDeviceToHost, st);
+        }
+        cudaMemcpyAsync(fill_all.data(), b_fill.p, b_fill.n, cudaMemcpyDeviceToHost, st);
+        cudaMemcpyAsync(below.data(), b_below.p, b_below.n, cudaMemcpyDeviceToHost, st);
+        if ((rc = check_cuda(cudaStreamSynchronize(st), "bracket sync 2"))) return rc;
         // ---- 3. verify the brackets, exact rounds over the candidates ----
         const int first_shift = (top_bit / RD_BITS) * RD_BITS;  // digits cover bits <= top_bit
         const uint64_t keep = first_shift + RD_BITS >= 64 ? 0ull : ~((1ull << (first_shift + RD_BITS)) - 1);
@@ -652,22 +683,22 @@ extern "C" int cs_rep_stats_impl(const double* d_resp, int32_t n_groups, int64_t
             const int64_t g = (int64_t)i / n_ranks;
             const size_t li = g * MAX_LISTS + list_of[i];
             const int64_t k = target[i];
-            if ((int64_t)fill[li] > cap[li] || (int64_t)below[li] > k || k >= (int64_t)(below[li] + fill[li])) {
+            if (overflow[li] || (int64_t)below[li] > k || k >= (int64_t)(below[li] + fill_all[li])) {
                 ok = false;
                 break;
             }
             slots[i].prefix = lo[li] & keep;  // bits shared by every candidate of the bracket
             slots[i].rank = k - (int64_t)below[li];
             slots[i].cand_off = off[li];
-            slots[i].cand_len = (int64_t)fill[li];
+            slots[i].cand_len = (int64_t)fill[li];  // this rank's candidates
         }
         if (!ok) continue;  // the sample missed a target (or overflowed): widen, retry
-        if ((rc = run_rounds(slots, b_cand.as<double>(), first_shift, st))) return rc;
+        if ((rc = run_rounds(slots, b_cand.as<double>(), first_shift, dist, st))) return rc;
         for (size_t i = 0; i < T; i++) memcpy(&out_values[i], &slots[i].prefix, 8);
         return CS_OK;
     }
     std::vector<double> vals;  // last resort: exact selection over everything
-    if ((rc = select_rows(d_resp, n_groups, rows_per_group, full, ldr, target, n_ranks, vals, st))) return rc;
+    if ((rc = select_rows(d_resp, n_groups, rows_per_group, full, ldr, target, n_ranks, vals, dist, st))) return rc;
     for (size_t i = 0; i < vals.size(); i++) out_values[i] = vals[i];
     return CS_OK;
 }

@@ -1,0 +1,109 @@
+"""Multi-GPU sweeps: replications sharded over one process per GPU.
+
+Replications are independent (chainserve sim.py:400-404 runs them in a
+process pool and merges order-independently), so each rank simulates a
+contiguous block of replication indices -- each keeps its reference spawn key
+(seed, rep), so results do not depend on the number of GPUs.  The only
+cross-GPU traffic is the final aggregation:
+
+* the per-replication summaries and busy times: one NCCL all-gather
+  (torch.distributed on device tensors);
+* the exact global quantiles: the engine's own NCCL communicator all-reduces
+  the radix-select histograms and bracket counts (cs_rep_stats_dist).
+
+Launch with torchrun (one rank per GPU), call ``init()`` once, then
+``run_sim_sharded(configs)``: every rank returns the same SimStats list, equal
+to ``run_sim_batch(configs)`` on one GPU.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from typing import Sequence
+
+import numpy as np
+
+from . import _native as N
+from .sim import SimConfig, SimStats, _require_supported, _stats_from
+
+_initialised = False
+
+
+def rank_world() -> tuple[int, int]:
+    import torch.distributed as dist
+
+    if dist.is_available() and dist.is_initialized():
+        return dist.get_rank(), dist.get_world_size()
+    return 0, 1
+
+
+def shard(total: int, rank: int, world: int) -> tuple[int, int]:
+    """Equal contiguous replication blocks: (begin, count) of this rank."""
+    if total % world:
+        raise ValueError(f"replications ({total}) must be divisible by the number of GPUs ({world})")
+    per = total // world
+    return rank * per, per
+
+
+def init() -> None:
+    """Create the engine's NCCL communicator over the torch.distributed group."""
+    global _initialised
+    import torch
+    import torch.distributed as dist
+
+    rank, world = rank_world()
+    lib = N.load()
+    if world == 1:
+        _initialised = True
+        return
+    uid = C.create_string_buffer(128)
+    if rank == 0:
+        N.check(lib.cs_nccl_unique_id(uid), "cs_nccl_unique_id")
+    t = torch.tensor(list(uid.raw), dtype=torch.uint8, device="cuda")
+    dist.broadcast(t, 0)
+    raw = bytes(t.cpu().tolist())
+    N.check(lib.cs_comm_init(raw, world, rank), "cs_comm_init")
+    _initialised = True
+
+
+def all_gather_rows(local: np.ndarray) -> np.ndarray:
+    """Concatenate equal-shape per-rank arrays in rank order (NCCL all-gather)."""
+    import torch
+    import torch.distributed as dist
+
+    rank, world = rank_world()
+    if world == 1:
+        return local
+    flat = np.ascontiguousarray(local).view(np.uint8).ravel()
+    t = torch.from_numpy(flat).to("cuda")
+    out = [torch.empty_like(t) for _ in range(world)]
+    dist.all_gather(out, t)
+    parts = [o.cpu().numpy().view(local.dtype).reshape(local.shape) for o in out]
+    return np.concatenate(parts, axis=1 if local.ndim >= 2 else 0)
+
+
+def run_sim_sharded(configs: Sequence[SimConfig]) -> list[SimStats]:
+    """run_sim_batch with the replications of every config split over the ranks."""
+    from .engine import SweepEngine
+
+    if not _initialised:
+        init()
+    c0 = configs[0]
+    for c in configs:
+        _require_supported(c)
+        if (c.horizon_jobs, c.warmup_fraction, c.seed, c.replications) != \
+                (c0.horizon_jobs, c0.warmup_fraction, c0.seed, c0.replications):
+            raise ValueError("configs must share horizon, warmup, seed and replications")
+        if c.collect_jobs:
+            raise NotImplementedError("collect_jobs is not supported for sharded sweeps")
+    rank, world = rank_world()
+    begin, count = shard(c0.replications, rank, world)
+    eng = SweepEngine([c.rates for c in configs], [c.capacities for c in configs],
+                      [c.workload.rate for c in configs], c0.horizon_jobs, c0.warmup_fraction,
+                      c0.seed, count, rep_begin=begin, distributed=world > 1,
+                      total_reps=c0.replications)
+    eng.step()
+    summ = all_gather_rows(eng.summaries())                       # [P, R]
+    busy = all_gather_rows(eng.busy())                            # [P, R, ldb]
+    order = eng.order_stats()
+    return [_stats_from(c, summ[p], busy[p], order[p], None) for p, c in enumerate(configs)]

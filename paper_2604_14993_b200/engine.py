@@ -37,7 +37,8 @@ class SweepEngine:
 
     def __init__(self, rates_list: Sequence[Sequence[float]], caps_list: Sequence[Sequence[int]],
                  lams: Sequence[float], n_jobs: int, warmup_fraction: float, seed: int, reps: int,
-                 rep_begin: int = 0, log1p_variant: int = -1, device: int | None = None):
+                 rep_begin: int = 0, log1p_variant: int = -1, device: int | None = None,
+                 distributed: bool = False, total_reps: int | None = None):
         import torch
 
         self.torch = torch
@@ -81,7 +82,9 @@ class SweepEngine:
         wsb = self.lib.cs_jffc_sim_workspace_bytes(self.P, reps, self.max_chains, self.max_cap, n_jobs)
         self.d_ws = torch.empty(max(wsb, 16), dtype=torch.uint8, device=dev)
         self.ws_bytes = wsb
-        N_total = reps * self.m
+        # sharded (distributed=True): ranks index the union of all shards' responses
+        self.distributed = distributed
+        N_total = (total_reps if distributed and total_reps else reps) * self.m
         self.rank_list = sorted({r for q in QUANTILES for r in _quantile_ranks(N_total, q)[:2]})
         self.ranks = np.asarray(self.rank_list * self.P, np.int64)
         self.out_vals = np.zeros(len(self.ranks), np.float64)
@@ -103,10 +106,10 @@ class SweepEngine:
         N.check(st, "cs_jffc_sim")
 
     def statistics(self):
-        st = self.lib.cs_rep_stats(self.d_resp.data_ptr(), self.P, self.R, self.m, self.ldr,
-                                   self.d_summ.data_ptr(), N.ptr(self.ranks, C.c_int64),
-                                   len(self.rank_list), N.ptr(self.out_vals, C.c_double), None,
-                                   self.stream.cuda_stream)
+        fn = self.lib.cs_rep_stats_dist if self.distributed else self.lib.cs_rep_stats
+        st = fn(self.d_resp.data_ptr(), self.P, self.R, self.m, self.ldr, self.d_summ.data_ptr(),
+                N.ptr(self.ranks, C.c_int64), len(self.rank_list), N.ptr(self.out_vals, C.c_double),
+                None, self.stream.cuda_stream)
         N.check(st, "cs_rep_stats")
 
     def step(self, timed: bool = False) -> StageTimes | None:
@@ -131,6 +134,9 @@ class SweepEngine:
     def summaries(self) -> np.ndarray:
         self.h_summ[:] = self.d_summ.cpu().numpy().view(N.SUMMARY_DTYPE)
         return self.h_summ.reshape(self.P, self.R)
+
+    def busy(self) -> np.ndarray:
+        return self.d_busy.cpu().numpy().reshape(self.P, self.R, self.ldb)
 
     def order_stats(self) -> list[dict]:
         k = len(self.rank_list)
