@@ -1,0 +1,107 @@
+#!/usr/bin/env python
+"""Composition throughput (BASELINE config 4): random 1000-server instances
+through GBP-CR block placement + GCA chain composition, composed instances/s.
+
+Instances: fleet(J=1000, L=80, seed=i) of SURVEY.md §8(d) (two-tier GPUs,
+RTT ~ U(5,60) ms), generated vectorised (compose_engine.fleet_soa, identical
+draws).  Two regimes (c=7, rho=0.7): moderate lambda=5 and full fleet
+lambda=1e9.  Prints one JSON line per regime, with the oracle port (C, all
+host threads via a process pool) timed on a bounded sample of the same
+instances and the GPU results checked against it on that sample.
+
+    python bench_compose.py [--instances 10000] [--regime moderate|full|both]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+from concurrent.futures import ProcessPoolExecutor
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+S_M, S_C, L, J = int(1.32e9), int(0.11e9), 80, 1000
+
+
+def _oracle_one(args):
+    seed, lam = args
+    from oracle import oracle as O
+    from paper_2604_14993_b200.compose_engine import fleet_soa
+
+    mem, tc, tp = fleet_soa(J, L, seed)
+    ids = [f"n{i:04d}" for i in range(J)]
+    st, g = O.gbp(mem, tc, tp, ids, L, S_M, S_C, 7, lam, 0.7)
+    st2, a = O.gca(mem, tc, tp, ids, L, S_M, S_C, g["first"], g["count"])
+    return seed, list(a["caps"]), [float(x) for x in a["times"]], int(a["n_edges"])
+
+
+def run(regime: str, n_inst: int, steps: int, cpu_sample: int):
+    import torch
+
+    from paper_2604_14993_b200.compose_engine import ComposeEngine, fleet_soa
+
+    lam = 5.0 if regime == "moderate" else 1e9
+    t0 = time.perf_counter()
+    parts = [fleet_soa(J, L, s) for s in range(n_inst)]
+    mem = np.concatenate([p[0] for p in parts])
+    tc = np.concatenate([p[1] for p in parts])
+    tp = np.concatenate([p[2] for p in parts])
+    gen_s = time.perf_counter() - t0
+    eng = ComposeEngine(mem, tc, tp, J, L, S_M, S_C, 7, lam, 0.7,
+                        max_chains=64 if regime == "moderate" else 512)
+    eng.run()
+    torch.cuda.synchronize()
+    times = [eng.run(timed=True) for _ in range(steps)]
+    gbp_ms = float(np.mean([t.gbp_ms for t in times]))
+    gca_ms = float(np.mean([t.gca_ms for t in times]))
+    res = eng.results()
+    assert (res["gbp_status"] == 0).all() and (res["gca_status"] == 0).all(), "engine status"
+    # CPU baseline + parity on a bounded sample
+    cores = os.cpu_count() or 1
+    sample = list(range(min(cpu_sample, n_inst)))
+    t0 = time.perf_counter()
+    with ProcessPoolExecutor(max_workers=cores) as ex:
+        ref = list(ex.map(_oracle_one, [(s, lam) for s in sample]))
+    cpu_s = time.perf_counter() - t0
+    for seed, caps, tms, ne in ref:
+        k = int(res["n_chains"][seed])
+        assert list(res["caps"][seed, :k]) == caps, seed
+        assert np.array_equal(res["times"][seed, :k].view(np.uint64), np.array(tms).view(np.uint64)), seed
+        assert int(res["n_edges"][seed]) == ne, seed
+    total_ms = gbp_ms + gca_ms
+    return {
+        "metric": "composed instances/sec (GBP-CR + GCA)", "regime": regime,
+        "value": n_inst / (total_ms / 1e3), "unit": "instances/s", "n_gpus": 1, "steps": steps,
+        "ms_per_step": total_ms, "stages_ms": {"gbp": gbp_ms, "gca": gca_ms},
+        "config": {"workload": f"config4: {n_inst} x fleet(J={J}, L={L}, seed=i), c=7, lambda={lam:g}, "
+                               "rho=0.7", "mean_chains": float(res["n_chains"].mean()),
+                   "mean_edges": float(res["n_edges"].mean()), "fleet_gen_s": gen_s},
+        "cpu_baseline": {"value": len(sample) / cpu_s, "unit": "instances/s", "cores": cores,
+                         "kind": "port", "sample": f"first {len(sample)} instances, oracle/cs_oracle.c "
+                                                   f"(heap Dijkstra, as cache_alloc.py) in {cpu_s:.2f} s"},
+        "parity": f"bit-exact caps/times/edge counts on {len(sample)} instances",
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--instances", type=int, default=10000)
+    ap.add_argument("--regime", default="both", choices=["moderate", "full", "both"])
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--cpu-sample", type=int, default=32)
+    a = ap.parse_args()
+    regimes = ["moderate", "full"] if a.regime == "both" else [a.regime]
+    for r in regimes:
+        n = a.instances if r == "moderate" else min(a.instances, 2000)
+        print(json.dumps(run(r, n, a.steps, a.cpu_sample if r == "moderate" else min(a.cpu_sample, 8))),
+              flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -452,6 +452,17 @@ static int select_rows(const double* d_resp, int64_t n_groups, int64_t rows_per_
         d_resp, n_rows, rv, ldr, rows_per_group, b_nl.as<int32_t>(), b_bk.as<uint32_t>(), b_off.as<int64_t>(),
         b_cap.as<int64_t>(), b_fill.as<unsigned long long>(), b_cand.as<double>());
     if ((rc = check_launch("compact_bucket_kernel"))) return rc;
+    if (dist) {  // candidates are this rank's values only: use the local counts
+        std::vector<unsigned long long> fill((size_t)MAX_LISTS * n_groups);
+        cudaMemcpyAsync(fill.data(), b_fill.p, b_fill.n, cudaMemcpyDeviceToHost, st);
+        if ((rc = check_cuda(cudaStreamSynchronize(st), "compact sync"))) return rc;
+        for (int64_t g = 0; g < n_groups; g++)
+            for (int q = 0; q < n_ranks; q++) {
+                SelSlot& s = slots[g * n_ranks + q];
+                for (int l = 0; l < nlist[g]; l++)
+                    if (off[g * MAX_LISTS + l] == s.cand_off) s.cand_len = (int64_t)fill[g * MAX_LISTS + l];
+            }
+    }
     if ((rc = run_rounds(slots, b_cand.as<double>(), 36, dist, st))) return rc;  // bits 47..0
     out.resize(slots.size());
     for (size_t i = 0; i < slots.size(); i++) memcpy(&out[i], &slots[i].prefix, 8);
