@@ -12,9 +12,9 @@
 // Quantiles need exact order statistics of each sweep point's merged
 // responses (the values np.quantile interpolates between).  An exact
 // sample-select whose only full read of the responses is the leaf-sum pass:
-//   1. sample = chunks of 32 consecutive responses every 1024 of each row
+//   1. sample = 4 consecutive responses (one sector) of every 128 of each row
 //      (1/32 of the bytes, spread over the whole run).  Exact sample order
-//      statistics at ranks k|S|/N -+ 5 sigma bracket each target: MSB radix
+//      statistics at ranks k|S|/N -+ 12 sigma bracket each target: MSB radix
 //      select on the IEEE bit patterns (responses >= +0, so bit order ==
 //      value order): 15-bit digit-0 histogram, compaction of the selected
 //      buckets, 12-bit digit rounds.
@@ -25,6 +25,8 @@
 //      the few candidates, starting below the bracket's common bit prefix.
 #include <cuda_runtime.h>
 #include <math.h>
+#include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -576,8 +578,11 @@ extern "C" int cs_rep_stats_impl(const double* d_resp, int32_t n_groups, int64_t
         return check_launch("tree_combine_kernel");
     };
     const RowView full{m, 40, 40};  // contiguous
-    const int64_t n_chunks = m / 1024, tail = std::min<int64_t>(32, m % 1024);
-    const RowView sample{n_chunks * 32 + tail, 5, 10};  // 32 of every 1024 responses
+    // one 32-byte sector (4 responses) of every 128: 1/32 of the bytes, and far
+    // less autocorrelated (queueing makes consecutive responses similar) than
+    // long chunks
+    const int64_t n_chunks = m / 128, tail = std::min<int64_t>(4, m % 128);
+    const RowView sample{n_chunks * 4 + tail, 2, 7};
     if (!want_ranks || N <= (1 << 20) || sample.len < 64) {
         if ((rc = leaf_pass(0, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr)) ||
             (rc = combine()))
@@ -599,7 +604,8 @@ extern "C" int cs_rep_stats_impl(const double* d_resp, int32_t n_groups, int64_t
         for (size_t i = 0; i < T; i++) {
             const double p = (double)target[i] / (double)N;
             const double ks = p * (double)NS;
-            const double delta = widen * (5.0 * sqrt(ks * (1.0 - p) + 1.0) + 16.0);
+            // 12 binomial sigmas: margin for the residual autocorrelation of the sample
+            const double delta = widen * (12.0 * sqrt(ks * (1.0 - p) + 1.0) + 64.0);
             r_lo[i] = std::max<int64_t>(0, (int64_t)floor(ks - delta));
             r_hi[i] = std::min<int64_t>(NS - 1, (int64_t)ceil(ks + delta));
         }
@@ -695,6 +701,11 @@ extern "C" int cs_rep_stats_impl(const double* d_resp, int32_t n_groups, int64_t
             const size_t li = g * MAX_LISTS + list_of[i];
             const int64_t k = target[i];
             if (overflow[li] || (int64_t)below[li] > k || k >= (int64_t)(below[li] + fill_all[li])) {
+                if (getenv("CS_DEBUG_STATS"))
+                    fprintf(stderr, "[cs_rep_stats] bracket miss: attempt %d slot %zu k=%lld below=%llu "
+                            "fill=%llu local=%llu cap=%lld ovf=%llu lo=%016llx hi=%016llx dist=%d\n",
+                            attempt, i, (long long)k, below[li], fill_all[li], fill[li], (long long)cap[li],
+                            overflow[li], (unsigned long long)lo[li], (unsigned long long)hi[li], (int)dist);
                 ok = false;
                 break;
             }
