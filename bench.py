@@ -129,6 +129,16 @@ def measured_peaks():
     return 6650.0, "fallback"
 
 
+def ncu_traffic(kernel: str, jobs: int, reps: int, points: int):
+    """DRAM bytes per launch of `kernel` from the committed ncu capture (same config only)."""
+    path = os.path.join(ROOT, "profiles", "r1_traffic.json")
+    if not os.path.exists(path) or (jobs, reps, points) != (100_000, 1024, 16):
+        return None
+    with open(path) as fh:
+        k = json.load(fh)["kernels"].get(kernel)
+    return None if k is None else k["dram_read_bytes"] + k["dram_write_bytes"]
+
+
 def cpu_baseline(rates, caps, lams, args, reps=None):
     """The oracle port (C, all host threads) on a bounded sample of the workload."""
     from oracle import oracle as O
@@ -320,7 +330,9 @@ def main():
             },
             "stages_ms": {"streams": streams_ms, "jffc_sim": sim_ms, "stats": stats_ms},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None, "kernel": "jffc_sim_reg_kernel",
+                         "frac": achieved / peak,
+                         "traffic": ncu_traffic("jffc_sim_reg_kernel", args.jobs, R, args.points),
+                         "algorithmic_bytes": alg_bytes, "kernel": "jffc_sim_reg_kernel",
                          "peak_source": peak_kind,
                          "note": "latency-bound serial event loops; see DESIGN.md roofline"},
             "cpu_baseline": cpu,
