@@ -67,6 +67,8 @@ int cs_exp_streams(const uint64_t* d_keys, int64_t n_streams, int64_t n_draws, d
 /* ------------------------------------------------------------------------ */
 /* JFFC simulation                                                            */
 /* ------------------------------------------------------------------------ */
+#define CS_STREAM_PAD 512 /* doubles of readable tail padding after the stream buffer */
+
 /* One sweep point: a composed system (chains chain_base..chain_base+K-1 of the
  * rates/caps arrays, rates descending) under Poisson arrivals of rate lam. */
 typedef struct {
@@ -97,6 +99,8 @@ typedef struct {
  * n_reps replications starting at rep_begin (of n_reps_total).  Chunk row r
  * reads stream row r of d_streams (2*n_jobs draws, row stride lds):
  * arrivals = cumsum((1/lam) * S[0:n]), sizes = S[n:2n].
+ * The stream buffer must stay readable CS_STREAM_PAD doubles past the last
+ * row (the simulator's cursors and prefetches run ahead without clamping).
  * Outputs are point-major, o = p*n_reps_total + rep_begin + r:
  *   d_responses[o*ldr + q]  q < n-warm, completion order (NULL: not stored;
  *                           ldr must be even -- rows are written with 16-byte stores)

@@ -294,7 +294,7 @@ int cs_run_sim_host(const cs_sim_point* points, int32_t n_points, const double* 
         (rc = b_rates.alloc(sizeof(double) * n_chain_entries, st)) ||
         (rc = b_caps.alloc(sizeof(int32_t) * n_chain_entries, st)) ||
         (rc = b_keys.alloc(sizeof(uint64_t) * 2 * chunk, st)) ||
-        (rc = b_S.alloc(sizeof(double) * lds * chunk, st)) ||
+        (rc = b_S.alloc(sizeof(double) * (lds * chunk + CS_STREAM_PAD), st)) ||
         (rc = b_resp.alloc(sizeof(double) * ldr * rows, st)) ||
         (rc = b_busy.alloc(sizeof(double) * ldb * rows, st)) ||
         (rc = b_summ.alloc(sizeof(cs_rep_summary) * rows, st)))

@@ -75,7 +75,7 @@ class SweepEngine:
                                         reps, N.ptr(keys, C.c_uint64)), "cs_philox_keys")
         self.h_keys = keys
         self.d_keys = torch.from_numpy(keys.view(np.int64)).to(dev)
-        self.d_S = torch.empty(reps * self.lds, dtype=f64, device=dev)
+        self.d_S = torch.empty(reps * self.lds + 512, dtype=f64, device=dev)  # + CS_STREAM_PAD
         self.d_resp = torch.empty(self.P * reps * self.ldr, dtype=f64, device=dev)
         self.d_busy = torch.empty(self.P * reps * self.ldb, dtype=f64, device=dev)
         self.d_summ = torch.empty(self.P * reps * C.sizeof(N.RepSummary), dtype=torch.uint8, device=dev)
