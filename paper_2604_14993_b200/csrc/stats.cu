@@ -40,7 +40,8 @@ constexpr int H0_BITS = 15;
 constexpr int H0_BINS = 1 << H0_BITS;
 constexpr int RD_BITS = 12;  // digit width of the selection rounds
 constexpr int RD_BINS = 1 << RD_BITS;
-constexpr int MAX_LISTS = 6;
+constexpr int MAX_LISTS = 6;   // quantile brackets per group
+constexpr int SEL_LISTS = 12;  // ranks per group of one exact selection (sample: both bracket ends)
 
 __device__ __forceinline__ uint64_t dbits(double v) { return (uint64_t)__double_as_longlong(v); }
 
@@ -126,9 +127,9 @@ __global__ void compact_bucket_kernel(const double* __restrict__ resp, int64_t n
     for (int64_t row = blockIdx.x; row < n_rows; row += gridDim.x) {
         const int64_t g = row / rows_per_group;
         const int nl = grp_nlist[g];
-        uint32_t bk[MAX_LISTS];
+        uint32_t bk[SEL_LISTS];
 #pragma unroll
-        for (int q = 0; q < MAX_LISTS; q++) bk[q] = q < nl ? grp_bucket[g * MAX_LISTS + q] : 0xffffffffu;
+        for (int q = 0; q < SEL_LISTS; q++) bk[q] = q < nl ? grp_bucket[g * SEL_LISTS + q] : 0xffffffffu;
         const double* __restrict__ a = resp + row * ldr;
         for (int64_t base = 0; base < rv.len; base += blockDim.x) {
             const int64_t s = base + threadIdx.x;
@@ -138,8 +139,8 @@ __global__ void compact_bucket_kernel(const double* __restrict__ resp, int64_t n
                 v = a[rv.phys(s)];
                 const uint32_t d0 = (uint32_t)(dbits(v) >> 48);
 #pragma unroll
-                for (int q = 0; q < MAX_LISTS; q++)
-                    if (bk[q] == d0) list = (int)(g * MAX_LISTS + q);
+                for (int q = 0; q < SEL_LISTS; q++)
+                    if (bk[q] == d0) list = (int)(g * SEL_LISTS + q);
             }
             append(list, v, fill, off, cap, cand);
         }
@@ -155,6 +156,55 @@ __device__ __forceinline__ int bracket_of(uint64_t w, const uint64_t* bl, const 
         if (w >= bl[q] && w <= bh[q]) list = (int)(g * MAX_LISTS + q);
     }
     return list;
+}
+
+// Bracket classification of one lane's 16 values (NB = bracket slots used;
+// unused slots have lo = ~0, hi = 0).  Counting uses the high 32 bits, which
+// decide exactly unless the high word lies inside a bracket's [lo, hi] high
+// words; those rare values take the exact 64-bit path and warp-aggregated
+// appends.
+template <int NB>
+__device__ __forceinline__ void classify(const double (&v)[16], int j, int main_end, const uint64_t* bl,
+                                         const uint64_t* bh, const uint32_t* bl_hw, const uint32_t* bh_hw,
+                                         uint32_t* cnt, int64_t g, unsigned long long* __restrict__ fill,
+                                         const int64_t* __restrict__ off, const int64_t* __restrict__ cap,
+                                         double* __restrict__ cand) {
+    uint32_t maybe = 0;
+#pragma unroll
+    for (int t = 0; t < 16; t++) {
+        const bool have = j + 8 * t < main_end;
+        const uint32_t hw = (uint32_t)(dbits(v[t]) >> 32);
+        bool in_any = false;
+#pragma unroll
+        for (int q = 0; q < NB; q++) {
+            cnt[q] += (have && hw < bl_hw[q]) ? 1u : 0u;
+            in_any |= hw >= bl_hw[q] && hw <= bh_hw[q];
+        }
+        if (have && in_any) maybe |= 1u << t;
+    }
+    while (__any_sync(0xffffffffu, maybe != 0)) {
+        int list = -1;
+        double w = 0.0;
+        if (maybe) {
+            const int t = __ffs(maybe) - 1;
+            maybe &= maybe - 1;
+#pragma unroll
+            for (int tt = 0; tt < 16; tt++)
+                if (tt == t) w = v[tt];
+            const uint64_t u = dbits(w);
+            const uint32_t hw = (uint32_t)(u >> 32);
+#pragma unroll
+            for (int q = 0; q < NB; q++) {
+                if (hw >= bl_hw[q] && hw <= bh_hw[q]) {
+                    if (u < bl[q])
+                        cnt[q]++;  // same high word, below lo
+                    else if (u <= bh[q])
+                        list = (int)(g * MAX_LISTS + q);
+                }
+            }
+        }
+        append(list, w, fill, off, cap, cand);
+    }
 }
 
 // The one full pass, one warp per replication row: numpy pairwise leaf sums
@@ -182,12 +232,15 @@ __global__ void __launch_bounds__(LB_WARPS * 32) row_stats_kernel(
     double stk[48];  // lane 0's split-tree stack (depth <= log2(m/64) + 2)
     for (int64_t row = (int64_t)blockIdx.x * LB_WARPS + warp; row < n_rows; row += (int64_t)gridDim.x * LB_WARPS) {
         const int64_t g = row / rows_per_group;
-        const int nl = do_bracket ? grp_nlist[g] : 0;
+        const int nl = do_bracket ? grp_nlist[g] : 0;  // warp-uniform, <= 3 after merging
         uint64_t bl[MAX_LISTS], bh[MAX_LISTS];
+        uint32_t bl_hw[MAX_LISTS], bh_hw[MAX_LISTS];
 #pragma unroll
         for (int q = 0; q < MAX_LISTS; q++) {
             bl[q] = q < nl ? lo[g * MAX_LISTS + q] : ~0ull;
             bh[q] = q < nl ? hi[g * MAX_LISTS + q] : 0ull;
+            bl_hw[q] = (uint32_t)(bl[q] >> 32);
+            bh_hw[q] = (uint32_t)(bh[q] >> 32);
         }
         uint32_t cnt[MAX_LISTS] = {0, 0, 0, 0, 0, 0};
         int sp = 0;
@@ -206,12 +259,10 @@ __global__ void __launch_bounds__(LB_WARPS * 32) row_stats_kernel(
             for (int t = 1; t < 16; t++)
                 if (j + 8 * t < main_end) acc = __dadd_rn(acc, v[t]);
             if (do_bracket) {
-#pragma unroll
-                for (int t = 0; t < 16; t++) {
-                    const bool have = j + 8 * t < main_end;
-                    const int list = have ? bracket_of(dbits(v[t]), bl, bh, cnt, g) : -1;
-                    append(list, v[t], fill, off, cap, cand);
-                }
+                if (nl <= 3)
+                    classify<3>(v, j, main_end, bl, bh, bl_hw, bh_hw, cnt, g, fill, off, cap, cand);
+                else
+                    classify<MAX_LISTS>(v, j, main_end, bl, bh, bl_hw, bh_hw, cnt, g, fill, off, cap, cand);
             }
             // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) in numpy's order
             const double s1 = __dadd_rn(acc, __shfl_down_sync(0xffffffffu, acc, 1));
@@ -410,8 +461,8 @@ static int select_rows(const double* d_resp, int64_t n_groups, int64_t rows_per_
         return CS_INTERNAL;
     }
     std::vector<int32_t> nlist(n_groups, 0);
-    std::vector<uint32_t> bucket((size_t)n_groups * MAX_LISTS, 0xffffffffu);
-    std::vector<int64_t> off((size_t)n_groups * MAX_LISTS, 0), cap((size_t)n_groups * MAX_LISTS, 0);
+    std::vector<uint32_t> bucket((size_t)n_groups * SEL_LISTS, 0xffffffffu);
+    std::vector<int64_t> off((size_t)n_groups * SEL_LISTS, 0), cap((size_t)n_groups * SEL_LISTS, 0);
     std::vector<SelSlot> slots((size_t)n_groups * n_ranks);
     int64_t total = 0;
     for (int64_t g = 0; g < n_groups; g++) {
@@ -426,27 +477,27 @@ static int select_rows(const double* d_resp, int64_t n_groups, int64_t rows_per_
             }
             int list = -1;
             for (int l = 0; l < nlist[g]; l++)
-                if (bucket[g * MAX_LISTS + l] == b) list = l;
+                if (bucket[g * SEL_LISTS + l] == b) list = l;
             if (list < 0) {
                 list = nlist[g]++;
-                bucket[g * MAX_LISTS + list] = b;
-                off[g * MAX_LISTS + list] = total;
-                cap[g * MAX_LISTS + list] = hg[b];
+                bucket[g * SEL_LISTS + list] = b;
+                off[g * SEL_LISTS + list] = total;
+                cap[g * SEL_LISTS + list] = hg[b];
                 total += hg[b];
             }
             SelSlot& s = slots[g * n_ranks + q];
             s.prefix = (uint64_t)b << 48;
             s.rank = rank - c;
-            s.cand_off = off[g * MAX_LISTS + list];
-            s.cand_len = cap[g * MAX_LISTS + list];
+            s.cand_off = off[g * SEL_LISTS + list];
+            s.cand_len = cap[g * SEL_LISTS + list];
         }
     }
     DBuf b_nl, b_bk, b_off, b_cap, b_fill, b_cand;
     if ((rc = b_nl.alloc(sizeof(int32_t) * n_groups, st)) ||
-        (rc = b_bk.alloc(sizeof(uint32_t) * MAX_LISTS * n_groups, st)) ||
-        (rc = b_off.alloc(sizeof(int64_t) * MAX_LISTS * n_groups, st)) ||
-        (rc = b_cap.alloc(sizeof(int64_t) * MAX_LISTS * n_groups, st)) ||
-        (rc = b_fill.alloc(sizeof(unsigned long long) * MAX_LISTS * n_groups, st)) ||
+        (rc = b_bk.alloc(sizeof(uint32_t) * SEL_LISTS * n_groups, st)) ||
+        (rc = b_off.alloc(sizeof(int64_t) * SEL_LISTS * n_groups, st)) ||
+        (rc = b_cap.alloc(sizeof(int64_t) * SEL_LISTS * n_groups, st)) ||
+        (rc = b_fill.alloc(sizeof(unsigned long long) * SEL_LISTS * n_groups, st)) ||
         (rc = b_cand.alloc(sizeof(double) * std::max<int64_t>(total, 1), st)))
         return rc;
     cudaMemcpyAsync(b_nl.p, nlist.data(), b_nl.n, cudaMemcpyHostToDevice, st);
@@ -459,14 +510,14 @@ static int select_rows(const double* d_resp, int64_t n_groups, int64_t rows_per_
         b_cap.as<int64_t>(), b_fill.as<unsigned long long>(), b_cand.as<double>());
     if ((rc = check_launch("compact_bucket_kernel"))) return rc;
     if (dist) {  // candidates are this rank's values only: use the local counts
-        std::vector<unsigned long long> fill((size_t)MAX_LISTS * n_groups);
+        std::vector<unsigned long long> fill((size_t)SEL_LISTS * n_groups);
         cudaMemcpyAsync(fill.data(), b_fill.p, b_fill.n, cudaMemcpyDeviceToHost, st);
         if ((rc = check_cuda(cudaStreamSynchronize(st), "compact sync"))) return rc;
         for (int64_t g = 0; g < n_groups; g++)
             for (int q = 0; q < n_ranks; q++) {
                 SelSlot& s = slots[g * n_ranks + q];
                 for (int l = 0; l < nlist[g]; l++)
-                    if (off[g * MAX_LISTS + l] == s.cand_off) s.cand_len = (int64_t)fill[g * MAX_LISTS + l];
+                    if (off[g * SEL_LISTS + l] == s.cand_off) s.cand_len = (int64_t)fill[g * SEL_LISTS + l];
             }
     }
     if ((rc = run_rounds(slots, b_cand.as<double>(), 36, dist, st))) return rc;  // bits 47..0
@@ -601,10 +652,21 @@ extern "C" int cs_rep_stats_impl(const double* d_resp, int32_t n_groups, int64_t
             r_lo[i] = std::max<int64_t>(0, (int64_t)floor(ks - delta));
             r_hi[i] = std::min<int64_t>(NS - 1, (int64_t)ceil(ks + delta));
         }
-        std::vector<double> v_lo, v_hi;
-        if ((rc = select_rows(d_resp, n_groups, rows_per_group, sample, ldr, r_lo, n_ranks, v_lo, dist, st)) ||
-            (rc = select_rows(d_resp, n_groups, rows_per_group, sample, ldr, r_hi, n_ranks, v_hi, dist, st)))
+        // both bracket ends of every target in ONE exact selection over the sample
+        std::vector<int64_t> r_both((size_t)n_groups * 2 * n_ranks);
+        for (int64_t g = 0; g < n_groups; g++)
+            for (int q = 0; q < n_ranks; q++) {
+                r_both[(g * 2 * n_ranks) + q] = r_lo[g * n_ranks + q];
+                r_both[(g * 2 * n_ranks) + n_ranks + q] = r_hi[g * n_ranks + q];
+            }
+        std::vector<double> v_both, v_lo(T), v_hi(T);
+        if ((rc = select_rows(d_resp, n_groups, rows_per_group, sample, ldr, r_both, 2 * n_ranks, v_both, dist, st)))
             return rc;
+        for (int64_t g = 0; g < n_groups; g++)
+            for (int q = 0; q < n_ranks; q++) {
+                v_lo[g * n_ranks + q] = v_both[g * 2 * n_ranks + q];
+                v_hi[g * n_ranks + q] = v_both[g * 2 * n_ranks + n_ranks + q];
+            }
         std::vector<int32_t> nlist(n_groups, 0);
         const size_t L6 = (size_t)n_groups * MAX_LISTS;
         std::vector<uint64_t> lo(L6, ~0ull), hi(L6, 0);
