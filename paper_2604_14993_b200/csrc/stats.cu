@@ -147,64 +147,33 @@ __global__ void compact_bucket_kernel(const double* __restrict__ resp, int64_t n
     }
 }
 
-__device__ __forceinline__ int bracket_of(uint64_t w, const uint64_t* bl, const uint64_t* bh, uint32_t* cnt,
-                                          int64_t g) {
+// Bracket state of one row (registers only: fixed sizes, static indices).
+template <int NB>
+struct Brackets {
+    uint64_t lo[NB], hi[NB];
+    uint32_t lo_hw[NB], hi_hw[NB];
+    uint32_t cnt[NB];
+};
+
+// Classify one value: counts values below each bracket and returns the
+// bracket list it falls in (or -1).  The high 32 bits decide unless they lie
+// within a bracket's high-word range; then the exact 64-bit compare runs.
+template <int NB>
+__device__ __forceinline__ int classify_one(Brackets<NB>& br, uint64_t u, bool have, int64_t g) {
+    const uint32_t hw = (uint32_t)(u >> 32);
     int list = -1;
 #pragma unroll
-    for (int q = 0; q < MAX_LISTS; q++) {
-        cnt[q] += w < bl[q];
-        if (w >= bl[q] && w <= bh[q]) list = (int)(g * MAX_LISTS + q);
-    }
-    return list;
-}
-
-// Bracket classification of one lane's 16 values (NB = bracket slots used;
-// unused slots have lo = ~0, hi = 0).  Counting uses the high 32 bits, which
-// decide exactly unless the high word lies inside a bracket's [lo, hi] high
-// words; those rare values take the exact 64-bit path and warp-aggregated
-// appends.
-template <int NB>
-__device__ __forceinline__ void classify(const double (&v)[16], int j, int main_end, const uint64_t* bl,
-                                         const uint64_t* bh, const uint32_t* bl_hw, const uint32_t* bh_hw,
-                                         uint32_t* cnt, int64_t g, unsigned long long* __restrict__ fill,
-                                         const int64_t* __restrict__ off, const int64_t* __restrict__ cap,
-                                         double* __restrict__ cand) {
-    uint32_t maybe = 0;
-#pragma unroll
-    for (int t = 0; t < 16; t++) {
-        const bool have = j + 8 * t < main_end;
-        const uint32_t hw = (uint32_t)(dbits(v[t]) >> 32);
-        bool in_any = false;
-#pragma unroll
-        for (int q = 0; q < NB; q++) {
-            cnt[q] += (have && hw < bl_hw[q]) ? 1u : 0u;
-            in_any |= hw >= bl_hw[q] && hw <= bh_hw[q];
+    for (int q = 0; q < NB; q++) {
+        const bool below_hw = hw < br.lo_hw[q];
+        const bool near = hw >= br.lo_hw[q] && hw <= br.hi_hw[q];
+        bool below = below_hw;
+        if (near) {  // rare
+            below = u < br.lo[q];
+            if (!below && u <= br.hi[q]) list = (int)(g * MAX_LISTS + q);
         }
-        if (have && in_any) maybe |= 1u << t;
+        br.cnt[q] += (have && below) ? 1u : 0u;
     }
-    while (__any_sync(0xffffffffu, maybe != 0)) {
-        int list = -1;
-        double w = 0.0;
-        if (maybe) {
-            const int t = __ffs(maybe) - 1;
-            maybe &= maybe - 1;
-#pragma unroll
-            for (int tt = 0; tt < 16; tt++)
-                if (tt == t) w = v[tt];
-            const uint64_t u = dbits(w);
-            const uint32_t hw = (uint32_t)(u >> 32);
-#pragma unroll
-            for (int q = 0; q < NB; q++) {
-                if (hw >= bl_hw[q] && hw <= bh_hw[q]) {
-                    if (u < bl[q])
-                        cnt[q]++;  // same high word, below lo
-                    else if (u <= bh[q])
-                        list = (int)(g * MAX_LISTS + q);
-                }
-            }
-        }
-        append(list, w, fill, off, cap, cand);
-    }
+    return have ? list : -1;
 }
 
 // The one full pass, one warp per replication row: numpy pairwise leaf sums
@@ -215,6 +184,7 @@ __device__ __forceinline__ void classify(const double (&v)[16], int j, int main_
 // merges) sits in shared memory.
 constexpr int LB_WARPS = 8;
 
+template <int NB>
 __global__ void __launch_bounds__(LB_WARPS * 32) row_stats_kernel(
     const double* __restrict__ resp, int64_t n_rows, int64_t rows_per_group, int64_t ldr, int64_t m,
     const int32_t* __restrict__ g_plan, int32_t L, cs_rep_summary* __restrict__ summ,
@@ -232,17 +202,16 @@ __global__ void __launch_bounds__(LB_WARPS * 32) row_stats_kernel(
     double stk[48];  // lane 0's split-tree stack (depth <= log2(m/64) + 2)
     for (int64_t row = (int64_t)blockIdx.x * LB_WARPS + warp; row < n_rows; row += (int64_t)gridDim.x * LB_WARPS) {
         const int64_t g = row / rows_per_group;
-        const int nl = do_bracket ? grp_nlist[g] : 0;  // warp-uniform, <= 3 after merging
-        uint64_t bl[MAX_LISTS], bh[MAX_LISTS];
-        uint32_t bl_hw[MAX_LISTS], bh_hw[MAX_LISTS];
+        const int nl = do_bracket ? grp_nlist[g] : 0;  // warp-uniform, <= NB (checked on the host)
+        Brackets<NB> br;
 #pragma unroll
-        for (int q = 0; q < MAX_LISTS; q++) {
-            bl[q] = q < nl ? lo[g * MAX_LISTS + q] : ~0ull;
-            bh[q] = q < nl ? hi[g * MAX_LISTS + q] : 0ull;
-            bl_hw[q] = (uint32_t)(bl[q] >> 32);
-            bh_hw[q] = (uint32_t)(bh[q] >> 32);
+        for (int q = 0; q < NB; q++) {
+            br.lo[q] = q < nl ? lo[g * MAX_LISTS + q] : ~0ull;
+            br.hi[q] = q < nl ? hi[g * MAX_LISTS + q] : 0ull;
+            br.lo_hw[q] = (uint32_t)(br.lo[q] >> 32);
+            br.hi_hw[q] = (uint32_t)(br.hi[q] >> 32);
+            br.cnt[q] = 0;
         }
-        uint32_t cnt[MAX_LISTS] = {0, 0, 0, 0, 0, 0};
         int sp = 0;
         const double* __restrict__ rowp = resp + row * ldr;
         for (int l0 = 0; l0 < L; l0 += 4) {
@@ -259,10 +228,11 @@ __global__ void __launch_bounds__(LB_WARPS * 32) row_stats_kernel(
             for (int t = 1; t < 16; t++)
                 if (j + 8 * t < main_end) acc = __dadd_rn(acc, v[t]);
             if (do_bracket) {
-                if (nl <= 3)
-                    classify<3>(v, j, main_end, bl, bh, bl_hw, bh_hw, cnt, g, fill, off, cap, cand);
-                else
-                    classify<MAX_LISTS>(v, j, main_end, bl, bh, bl_hw, bh_hw, cnt, g, fill, off, cap, cand);
+#pragma unroll
+                for (int t = 0; t < 16; t++) {
+                    const int list = classify_one<NB>(br, dbits(v[t]), j + 8 * t < main_end, g);
+                    if (__any_sync(0xffffffffu, list >= 0)) append(list, v[t], fill, off, cap, cand);
+                }
             }
             // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) in numpy's order
             const double s1 = __dadd_rn(acc, __shfl_down_sync(0xffffffffu, acc, 1));
@@ -277,7 +247,10 @@ __global__ void __launch_bounds__(LB_WARPS * 32) row_stats_kernel(
                 const bool have = j == 0 && idx < len;
                 const double w = have ? a[idx] : 0.0;
                 if (have) res = __dadd_rn(res, w);
-                if (do_bracket) append(have ? bracket_of(dbits(w), bl, bh, cnt, g) : -1, w, fill, off, cap, cand);
+                if (do_bracket) {
+                    const int list = classify_one<NB>(br, dbits(w), have, g);
+                    append(list, w, fill, off, cap, cand);
+                }
             }
             // leaves l0..l0+3 (lanes 0, 8, 16, 24) into lane 0's stack, in order
             const double r1 = __shfl_sync(0xffffffffu, res, 8);
@@ -304,8 +277,8 @@ __global__ void __launch_bounds__(LB_WARPS * 32) row_stats_kernel(
         }
         if (do_bracket) {
 #pragma unroll
-            for (int q = 0; q < MAX_LISTS; q++) {
-                uint32_t c = cnt[q];
+            for (int q = 0; q < NB; q++) {
+                uint32_t c = br.cnt[q];
                 for (int d = 16; d > 0; d >>= 1) c += __shfl_down_sync(0xffffffffu, c, d);
                 if (lane == 0 && q < nl && c) atomicAdd(&below[g * MAX_LISTS + q], (unsigned long long)c);
             }
@@ -608,15 +581,23 @@ extern "C" int cs_rep_stats_impl(const double* d_resp, int32_t n_groups, int64_t
         cudaMemcpyAsync(b_plan.p, h.data(), smem, cudaMemcpyHostToDevice, st);
         if ((rc = check_cuda(cudaStreamSynchronize(st), "plan upload"))) return rc;  // h dies here
     }
-    cudaFuncSetAttribute(row_stats_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 16));
+    cudaFuncSetAttribute(row_stats_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 16));
+    cudaFuncSetAttribute(row_stats_kernel<MAX_LISTS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)std::max<size_t>(smem, 16));
     const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((n_rows + LB_WARPS - 1) / LB_WARPS,
                                                                    (int64_t)sm_count() * 8));
+    int max_brackets = 0;  // set per bracket attempt; selects the kernel instance
     auto leaf_pass = [&](int do_bracket, const int32_t* nl, const uint64_t* lo, const uint64_t* hi,
                          const int64_t* off, const int64_t* cap, unsigned long long* fill,
                          unsigned long long* below, double* cand) {
-        row_stats_kernel<<<blocks, LB_WARPS * 32, std::max<size_t>(smem, 16), st>>>(
-            d_resp, n_rows, rows_per_group, ldr, m, b_plan.as<int32_t>(), L, d_summ, d_row_sums, do_bracket,
-            nl, lo, hi, off, cap, fill, below, cand);
+        if (max_brackets <= 3)
+            row_stats_kernel<3><<<blocks, LB_WARPS * 32, std::max<size_t>(smem, 16), st>>>(
+                d_resp, n_rows, rows_per_group, ldr, m, b_plan.as<int32_t>(), L, d_summ, d_row_sums, do_bracket,
+                nl, lo, hi, off, cap, fill, below, cand);
+        else
+            row_stats_kernel<MAX_LISTS><<<blocks, LB_WARPS * 32, std::max<size_t>(smem, 16), st>>>(
+                d_resp, n_rows, rows_per_group, ldr, m, b_plan.as<int32_t>(), L, d_summ, d_row_sums, do_bracket,
+                nl, lo, hi, off, cap, fill, below, cand);
         return check_launch("row_stats_kernel");
     };
     auto combine = [&]() { return CS_OK; };  // the tree is combined on chip
@@ -721,6 +702,7 @@ extern "C" int cs_rep_stats_impl(const double* d_resp, int32_t n_groups, int64_t
         cudaMemcpyAsync(b_cap.p, cap.data(), b_cap.n, cudaMemcpyHostToDevice, st);
         cudaMemsetAsync(b_fill.p, 0, b_fill.n, st);
         cudaMemsetAsync(b_below.p, 0, b_below.n, st);
+        max_brackets = *std::max_element(nlist.begin(), nlist.end());
         if ((rc = leaf_pass(1, b_nl.as<int32_t>(), b_lo.as<uint64_t>(), b_hi.as<uint64_t>(), b_off.as<int64_t>(),
                             b_cap.as<int64_t>(), b_fill.as<unsigned long long>(), b_below.as<unsigned long long>(),
                             b_cand.as<double>())))
