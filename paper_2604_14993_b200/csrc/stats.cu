@@ -159,21 +159,21 @@ struct Brackets {
 // bracket list it falls in (or -1).  The high 32 bits decide unless they lie
 // within a bracket's high-word range; then the exact 64-bit compare runs.
 template <int NB>
-__device__ __forceinline__ int classify_one(Brackets<NB>& br, uint64_t u, bool have, int64_t g) {
+__device__ __forceinline__ int classify_one(Brackets<NB>& br, uint64_t u, bool have) {
     const uint32_t hw = (uint32_t)(u >> 32);
-    int list = -1;
+    int slot = -1;
 #pragma unroll
     for (int q = 0; q < NB; q++) {
         const bool below_hw = hw < br.lo_hw[q];
         const bool near = hw >= br.lo_hw[q] && hw <= br.hi_hw[q];
         bool below = below_hw;
-        if (near) {  // rare
+        if (near) {  // rare: exact 64-bit compare
             below = u < br.lo[q];
-            if (!below && u <= br.hi[q]) list = (int)(g * MAX_LISTS + q);
+            if (!below && u <= br.hi[q]) slot = q;
         }
         br.cnt[q] += (have && below) ? 1u : 0u;
     }
-    return have ? list : -1;
+    return have ? slot : -1;
 }
 
 // The one full pass, one warp per replication row: numpy pairwise leaf sums
@@ -228,10 +228,27 @@ __global__ void __launch_bounds__(LB_WARPS * 32) row_stats_kernel(
             for (int t = 1; t < 16; t++)
                 if (j + 8 * t < main_end) acc = __dadd_rn(acc, v[t]);
             if (do_bracket) {
+                uint32_t hit = 0;     // bit t: value t falls inside a bracket
+                uint64_t which = 0;   // its bracket slot, 4 bits per value
 #pragma unroll
                 for (int t = 0; t < 16; t++) {
-                    const int list = classify_one<NB>(br, dbits(v[t]), j + 8 * t < main_end, g);
-                    if (__any_sync(0xffffffffu, list >= 0)) append(list, v[t], fill, off, cap, cand);
+                    const int q = classify_one<NB>(br, dbits(v[t]), j + 8 * t < main_end);
+                    if (q >= 0) {
+                        hit |= 1u << t;
+                        which |= (uint64_t)q << (4 * t);
+                    }
+                }
+                // the rare candidates: one vote per 16 values, re-read from L1
+                while (__any_sync(0xffffffffu, hit != 0)) {
+                    int list = -1;
+                    double w = 0.0;
+                    if (hit) {
+                        const int t = __ffs(hit) - 1;
+                        hit &= hit - 1;
+                        w = __ldg(a + j + 8 * t);
+                        list = (int)(g * MAX_LISTS + ((which >> (4 * t)) & 15));
+                    }
+                    append(list, w, fill, off, cap, cand);
                 }
             }
             // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) in numpy's order
@@ -248,8 +265,8 @@ __global__ void __launch_bounds__(LB_WARPS * 32) row_stats_kernel(
                 const double w = have ? a[idx] : 0.0;
                 if (have) res = __dadd_rn(res, w);
                 if (do_bracket) {
-                    const int list = classify_one<NB>(br, dbits(w), have, g);
-                    append(list, w, fill, off, cap, cand);
+                    const int q = classify_one<NB>(br, dbits(w), have);
+                    append(q >= 0 ? (int)(g * MAX_LISTS + q) : -1, w, fill, off, cap, cand);
                 }
             }
             // leaves l0..l0+3 (lanes 0, 8, 16, 24) into lane 0's stack, in order
