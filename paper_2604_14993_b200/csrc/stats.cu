@@ -214,6 +214,17 @@ __global__ void __launch_bounds__(LB_WARPS * 32) row_stats_kernel(
         }
         int sp = 0;
         const double* __restrict__ rowp = resp + row * ldr;
+        // software pipeline: the next leaf group's loads are in flight while
+        // this group's split-tree merges run
+        double nv[16];
+        {
+            const int leaf = sub;
+            const int len = leaf < L ? leaf_len[leaf] : 0;
+            const double* __restrict__ a = rowp + (leaf < L ? leaf_off[leaf] : 0);
+            const int main_end = len >= 8 ? len - len % 8 : 0;
+#pragma unroll
+            for (int t = 0; t < 16; t++) nv[t] = (j + 8 * t < main_end) ? __ldg(a + j + 8 * t) : 0.0;
+        }
         for (int l0 = 0; l0 < L; l0 += 4) {
             const int leaf = l0 + sub;
             const bool valid = leaf < L;
@@ -222,7 +233,15 @@ __global__ void __launch_bounds__(LB_WARPS * 32) row_stats_kernel(
             const int main_end = len >= 8 ? len - len % 8 : 0;
             double v[16];
 #pragma unroll
-            for (int t = 0; t < 16; t++) v[t] = (j + 8 * t < main_end) ? __ldg(a + j + 8 * t) : 0.0;
+            for (int t = 0; t < 16; t++) v[t] = nv[t];
+            {
+                const int nleaf = leaf + 4;
+                const int nlen = nleaf < L ? leaf_len[nleaf] : 0;
+                const double* __restrict__ na = rowp + (nleaf < L ? leaf_off[nleaf] : 0);
+                const int nmain = nlen >= 8 ? nlen - nlen % 8 : 0;
+#pragma unroll
+                for (int t = 0; t < 16; t++) nv[t] = (j + 8 * t < nmain) ? __ldg(na + j + 8 * t) : 0.0;
+            }
             double acc = v[0];
 #pragma unroll
             for (int t = 1; t < 16; t++)
