@@ -129,19 +129,51 @@ def test_sweep_matches_oracle_bit_exact(eng, oracle):
             assert same_float(v, merged[rank]), (p, rank)
 
 
-def test_generic_kernel_large_capacity(eng, oracle):
-    """K=12 chains, C=40: exercises the generic (workspace heap) kernel."""
-    rates = tuple(sorted((1.0 / (1 + 0.37 * k) for k in range(12)), reverse=True))
-    caps = tuple(1 + (k * 7) % 5 for k in range(12))
+def _chain_set(K, C, seed):
+    rng = np.random.default_rng(seed)
+    rates = tuple(sorted((float(x) for x in rng.uniform(0.2, 2.0, K)), reverse=True))
+    caps = [1] * K
+    for _ in range(C - K):
+        caps[int(rng.integers(K))] += 1
+    return rates, tuple(caps)
+
+
+# (K, C) per kernel path: warp kernel SPL x KPL variants, then the generic
+# (workspace heap) kernel beyond 512 slots
+LARGE_CASES = [(3, 20), (12, 40), (40, 100), (70, 200), (20, 400), (2, 600)]
+
+
+@pytest.mark.parametrize("K,C", LARGE_CASES)
+def test_large_composition_kernels(eng, oracle, K, C):
+    """Compositions beyond the register kernel (K > 8 or C > 16): warp-per-
+    replication kernel, and the generic kernel for C > 512."""
+    rates, caps = _chain_set(K, C, K * 1000 + C)
     lam = 0.9 * sum(r * c for r, c in zip(rates, caps))
-    res = eng.simulate_sweep([rates], [caps], [lam], 8000, 0.1, 3, 6, return_responses=True,
+    n, R = 6000, 5
+    res = eng.simulate_sweep([rates], [caps], [lam], n, 0.1, 3, R, return_responses=True,
                              collect_jobs=True)
-    for r in range(6):
-        o = oracle.simulate_once(rates, caps, lam, 8000, 0.1, 3, r, collect_jobs=True)
-        assert np.array_equal(bits(res.responses[0, r]), bits(o["responses"]))
-        assert np.array_equal(bits(res.jobs[0, r]), bits(o["jobs"]))
+    for r in range(R):
+        o = oracle.simulate_once(rates, caps, lam, n, 0.1, 3, r, collect_jobs=True)
+        assert np.array_equal(bits(res.responses[0, r]), bits(o["responses"])), r
+        assert np.array_equal(bits(res.jobs[0, r]), bits(o["jobs"])), r
+        assert np.array_equal(bits(res.busy[0][r, :K]), bits(o["busy_time_s"])), r
         for f in REP_FIELDS:
-            assert same_float(res.summaries[0, r][f], o[f]), f
+            assert same_float(res.summaries[0, r][f], o[f]), (r, f)
+
+
+def test_warp_kernel_mixed_points(eng, oracle):
+    """Several compositions of different K/C (and one register-sized one) in
+    one launch: the kernel is sized by the largest, smaller points pad."""
+    sets = [_chain_set(5, 30, 1), _chain_set(1, 7, 2), _chain_set(34, 87, 3)]
+    lams = [0.7 * sum(r * c for r, c in zip(*s)) for s in sets]
+    n, R = 4000, 4
+    res = eng.simulate_sweep([s[0] for s in sets], [s[1] for s in sets], lams, n, 0.1, 11, R,
+                             return_responses=True)
+    for p, (rates, caps) in enumerate(sets):
+        for r in range(R):
+            o = oracle.simulate_once(rates, caps, lams[p], n, 0.1, 11, r)
+            assert np.array_equal(bits(res.responses[p, r]), bits(o["responses"])), (p, r)
+            assert np.array_equal(bits(res.busy[p][r, :len(rates)]), bits(o["busy_time_s"])), (p, r)
 
 
 def _compose_inputs(c):
