@@ -36,6 +36,7 @@ extern "C" {
 #define CS_INTERNAL 3     /* AssertionError (cache_alloc.py:119,133)       */
 #define CS_ERR_CUDA 4     /* CUDA runtime failure / no device              */
 #define CS_UNSUPPORTED 5  /* NotImplementedError (mode outside the path)   */
+#define CS_UNSTABLE 6     /* UnstableError (analysis.py:96-97,132-133)     */
 
 const char* cs_version(void);
 const char* cs_last_error(void);
@@ -218,6 +219,49 @@ int cs_gca_batch(const cs_compose_point* d_points, int32_t n_points, int32_t max
                  int32_t max_chains, int32_t max_hops, int32_t* d_chain_srv,
                  int32_t* d_chain_len, int32_t* d_caps, double* d_times, int32_t* d_n_chains,
                  int64_t* d_n_edges, int32_t* d_status, void* stream);
+
+/* ---- occupancy bounds (analysis.py:67-147): the capacity-sweep caller ---- */
+
+/* One composed system: chains chain_base..+n_chains-1 of d_rates/d_caps
+ * (rates descending, as ChainRates), arrival rate lam. */
+typedef struct {
+    int32_t n_chains;
+    int32_t chain_base;
+    double lam;
+} cs_bound_point;
+
+typedef struct {
+    double lower_occupancy;   /* birth-death with death_rate_bounds()[0]  */
+    double upper_occupancy;   /* birth-death with death_rate_bounds()[1]  */
+    double lower_response_s;  /* lower_occupancy / lam (Little)           */
+    double upper_response_s;
+    double total_rate;        /* sum(r*c), CPython float sum (analysis.py:60) */
+    int32_t total_capacity;
+    int32_t status;           /* CS_OK, or CS_UNSTABLE when lam >= total_rate */
+} cs_bounds_out;
+
+/* occupancy_bounds() for every point (replaces analysis.py:121-147 per
+ * call; bound_curve analysis.py:270-297 batches the capacity sweep through
+ * it).  d_workspace: n_points * 2 * (max_capacity + 1) doubles. */
+int cs_occupancy_bounds(const cs_bound_point* d_points, int32_t n_points, const double* d_rates,
+                        const int32_t* d_caps, int32_t max_capacity, double* d_workspace,
+                        cs_bounds_out* d_out, void* stream);
+
+/* birth_death_mean_occupancy() (analysis.py:84-109) with explicit death
+ * rates d_death[base .. base+n_states-1] and total_rate; lam < total_rate
+ * and all death rates > 0 are the caller's checks (ValueError/UnstableError
+ * raised before the call).  d_workspace: n_points * (max_states + 1)
+ * doubles. */
+typedef struct {
+    int32_t n_states;
+    int32_t base;
+    double lam;
+    double total_rate;
+} cs_bd_point;
+
+int cs_birth_death_occupancy(const cs_bd_point* d_points, int32_t n_points,
+                             const double* d_death, int32_t max_states, double* d_workspace,
+                             double* d_out, void* stream);
 
 #ifdef __cplusplus
 }

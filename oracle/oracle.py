@@ -266,3 +266,62 @@ def gca(mem, tau_c, tau_p, ids, L, s_m, s_c, first, count, residual=None):
     chains = [tuple(int(x) for x in members[offs[k]:offs[k + 1]]) for k in range(K)]
     return st, dict(chains=chains, caps=caps[:K].copy(), times=times[:K].copy(),
                     n_edges=ne.value)
+
+
+# ---- occupancy bounds (analysis.py:67-147), numpy restatement -------------
+
+def death_rates(rates, caps):
+    """death_rate_bounds(rates, n) for n = 1..C (analysis.py:67-81): arrays
+    (fast, slow) of the sequential per-chain float sums."""
+    C_tot = int(sum(caps))
+    fast = np.zeros(C_tot)
+    slow = np.zeros(C_tot)
+    for n in range(1, C_tot + 1):
+        u = lo = 0.0
+        ahead, behind = 0, C_tot
+        for mu, c in zip(rates, caps):
+            u += mu * min(c, max(n - ahead, 0))
+            ahead += c
+            behind -= c
+            lo += mu * min(c, max(n - behind, 0))
+        fast[n - 1], slow[n - 1] = u, lo
+    return fast, slow
+
+
+def _logsumexp(a):
+    """scipy 1.18 special.logsumexp for a 1-D real array without weights:
+    maximal terms split out, log1p(s/m) + log(m) + max."""
+    a = np.asarray(a, np.float64)
+    amax = a.max()
+    is_max = a == amax
+    m = float(is_max.sum())
+    s = np.exp(np.where(is_max, -np.inf, a) - amax).sum()
+    if s != 0:
+        s = s / m
+    return np.log1p(s) + np.log(m) + amax
+
+
+def birth_death_mean_occupancy(lam, death, nu):
+    """analysis.py:84-109 (caller checks lam < nu, death > 0)."""
+    d = np.asarray(death, np.float64)
+    C_tot = d.size
+    rho = lam / nu
+    log_w = np.concatenate(([0.0], np.cumsum(np.log(lam) - np.log(d))))
+    tail = log_w[C_tot] + math.log(nu) - math.log(nu - lam)
+    log_z = _logsumexp(np.concatenate((log_w[:C_tot], [tail])))
+    n = np.arange(1, C_tot)
+    head = float(np.sum(n * np.exp(log_w[1:C_tot] - log_z))) if C_tot > 1 else 0.0
+    queued = math.exp(log_w[C_tot] - log_z) * (rho / (1 - rho) ** 2 + C_tot / (1 - rho))
+    return head + queued
+
+
+def occupancy_bounds(rates, caps, lam):
+    """analysis.py:121-147 -> (lower_occ, upper_occ, lower_resp, upper_resp),
+    or None when lam >= total rate (UnstableError in the reference)."""
+    nu = sum(r * c for r, c in zip(rates, caps))
+    if lam >= nu:
+        return None
+    fast, slow = death_rates(rates, caps)
+    lo = birth_death_mean_occupancy(lam, fast, nu)
+    hi = birth_death_mean_occupancy(lam, slow, nu)
+    return lo, hi, lo / lam, hi / lam

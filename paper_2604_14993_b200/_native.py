@@ -11,11 +11,11 @@ import os
 
 import numpy as np
 
-from .errors import InfeasibleError
+from .errors import InfeasibleError, UnstableError
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libchainserve_b200.so")
 
-CS_OK, CS_INFEASIBLE, CS_INVALID, CS_INTERNAL, CS_ERR_CUDA, CS_UNSUPPORTED = range(6)
+CS_OK, CS_INFEASIBLE, CS_INVALID, CS_INTERNAL, CS_ERR_CUDA, CS_UNSUPPORTED, CS_UNSTABLE = range(7)
 
 
 class NativeUnavailable(RuntimeError):
@@ -46,6 +46,19 @@ class ComposePoint(C.Structure):
     ]
 
 
+class BoundPoint(C.Structure):
+    _fields_ = [("n_chains", C.c_int32), ("chain_base", C.c_int32), ("lam", C.c_double)]
+
+
+class BdPoint(C.Structure):
+    _fields_ = [("n_states", C.c_int32), ("base", C.c_int32), ("lam", C.c_double),
+                ("total_rate", C.c_double)]
+
+
+BOUNDS_DTYPE = np.dtype([("lower_occupancy", "<f8"), ("upper_occupancy", "<f8"),
+                         ("lower_response_s", "<f8"), ("upper_response_s", "<f8"),
+                         ("total_rate", "<f8"), ("total_capacity", "<i4"), ("status", "<i4")])
+
 SUMMARY_DTYPE = np.dtype([(name, np.float64 if ct is C.c_double else np.int64)
                           for name, ct in RepSummary._fields_])
 assert SUMMARY_DTYPE.itemsize == C.sizeof(RepSummary)
@@ -54,7 +67,8 @@ EXPORTS = (
     "cs_version", "cs_last_error", "cs_host_log1p_variant", "cs_device_count", "cs_launch_count",
     "cs_philox_keys", "cs_exp_streams", "cs_jffc_sim", "cs_jffc_sim_workspace_bytes",
     "cs_rep_stats", "cs_rep_stats_dist", "cs_run_sim_host", "cs_gbp_batch", "cs_gca_batch",
-    "cs_nccl_unique_id", "cs_comm_init", "cs_comm_destroy",
+    "cs_nccl_unique_id", "cs_comm_init", "cs_comm_destroy", "cs_occupancy_bounds",
+    "cs_birth_death_occupancy",
 )
 
 _lib = None
@@ -97,6 +111,8 @@ def load(require_device: bool = True):
         L.cs_gbp_batch.argtypes = [vp, C.c_int32, C.c_int32] + [vp] * 14 + [vp]
         L.cs_gca_batch.argtypes = [vp, C.c_int32, C.c_int32, C.c_int32] + [vp] * 7 + \
             [C.c_int32, C.c_int32] + [vp] * 7 + [vp]
+        L.cs_occupancy_bounds.argtypes = [vp, C.c_int32, vp, vp, C.c_int32, vp, vp, vp]
+        L.cs_birth_death_occupancy.argtypes = [vp, C.c_int32, vp, C.c_int32, vp, vp, vp]
         _lib = L
     if require_device and _lib.cs_device_count() == 0:
         raise NativeUnavailable("no CUDA device visible: the chainserve B200 engine has no CPU path")
@@ -119,6 +135,8 @@ def check(status: int, what: str) -> None:
         raise AssertionError(msg)
     if status == CS_UNSUPPORTED:
         raise NotImplementedError(msg)
+    if status == CS_UNSTABLE:
+        raise UnstableError(msg)
     raise NativeUnavailable(msg)
 
 

@@ -198,30 +198,7 @@ __device__ bool lex_less(const GcaNode* __restrict__ nd, int u1, int u2, int v) 
     return nd[a].ord < nd[b].ord;
 }
 
-// Neumaier-compensated running sum, CPython >= 3.12 builtin sum() of floats.
-struct PySum {
-    double f, c;
-    bool started;
-    __device__ void init() {
-        f = 0.0;
-        c = 0.0;
-        started = false;
-    }
-    __device__ void add(double x) {
-        if (!started) {
-            f = x;  // int 0 + x
-            started = true;
-            return;
-        }
-        const double t = __dadd_rn(f, x);
-        if (fabs(f) >= fabs(x))
-            c = __dadd_rn(c, __dadd_rn(__dsub_rn(f, t), x));
-        else
-            c = __dadd_rn(c, __dadd_rn(__dsub_rn(x, t), f));
-        f = t;
-    }
-    __device__ double result() const { return (c != 0.0 && isfinite(c)) ? __dadd_rn(f, c) : f; }
-};
+// PySum (cs_internal.cuh): CPython >= 3.12 builtin sum() of floats.
 
 __global__ void __launch_bounds__(512) gca_kernel(
     const cs_compose_point* __restrict__ pts, const int64_t* __restrict__ mem,

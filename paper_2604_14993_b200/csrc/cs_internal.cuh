@@ -47,4 +47,31 @@ int allreduce_max_u64(void* buf, size_t count, cudaStream_t st);
 // Python-semantics helpers (no contraction; explicit IEEE round-to-nearest).
 __device__ __forceinline__ double py_div(double a, double b) { return __ddiv_rn(a, b); }
 
+// CPython 3.12 sum() of floats: Neumaier compensated summation starting from
+// int 0 (Python/bltinmodule.c builtin_sum_impl), used for chain service
+// times (model.py:204) and total rates (analysis.py:60).
+struct PySum {
+    double f, c;
+    bool started;
+    __device__ void init() {
+        f = 0.0;
+        c = 0.0;
+        started = false;
+    }
+    __device__ void add(double x) {
+        if (!started) {
+            f = x;  // int 0 + x
+            started = true;
+            return;
+        }
+        const double t = __dadd_rn(f, x);
+        if (fabs(f) >= fabs(x))
+            c = __dadd_rn(c, __dadd_rn(__dsub_rn(f, t), x));
+        else
+            c = __dadd_rn(c, __dadd_rn(__dsub_rn(x, t), f));
+        f = t;
+    }
+    __device__ double result() const { return (c != 0.0 && isfinite(c)) ? __dadd_rn(f, c) : f; }
+};
+
 }  // namespace cs
