@@ -121,6 +121,74 @@ int cs_jffc_sim(const cs_sim_point* d_points, int32_t n_points, const double* d_
 int64_t cs_jffc_sim_workspace_bytes(int32_t n_points, int32_t n_reps, int32_t max_chains,
                                     int32_t max_capacity, int64_t n_jobs);
 
+/* ---- the rest of run_sim's signature ---------- */
+/* _simulate_once for the dedicated-queue baseline policies (sim.py:104-117,
+ * 279-286), the sampled and trace workloads (sim.py:161-178,199-203,
+ * workload.py:124-167) and the time-horizon Poisson mode (sim.py:146-158,
+ * 187-190).  One warp per (point, replication); K <= 256, C <= 512. */
+#define CS_POLICY_JFFC 0
+#define CS_POLICY_JSQ 1
+#define CS_POLICY_SA_JSQ 2
+#define CS_POLICY_JIQ 3
+#define CS_POLICY_SED 4
+
+#define CS_WL_POISSON 0  /* streams: gaps S[0:n], sizes S[n:2n]            */
+#define CS_WL_HORIZON 1  /* streams: 4096-gap blocks cumsum(block)+total, then
+                            sizes; arrivals <= t_end, at most n_jobs        */
+#define CS_WL_SAMPLED 2  /* arrivals[n], sizes[n] shared by all replications */
+#define CS_WL_TRACE 3    /* arrivals[n], tokens_in/out[n]; per-chain hops   */
+
+/* per-replication status (d_rep_status) */
+#define CS_REP_QUEUE_OVERFLOW 16  /* a dedicated queue exceeded queue_capacity */
+#define CS_REP_EMPTY_HORIZON 17   /* no arrival inside the time horizon          */
+#define CS_REP_WARMUP_ALL 18      /* warm-up consumed every arrival              */
+
+typedef struct {
+    const cs_sim_point* points;   /* lam used by CS_WL_POISSON / CS_WL_HORIZON */
+    int32_t n_points;
+    int32_t policy;               /* CS_POLICY_*                              */
+    int32_t workload;             /* CS_WL_*                                  */
+    int32_t max_chains, max_capacity;
+    const double* rates;          /* chains at points[p].chain_base           */
+    const int32_t* caps;
+    const double* streams;        /* CS_WL_POISSON / CS_WL_HORIZON            */
+    int64_t lds;
+    double horizon_time_s;        /* CS_WL_HORIZON: t_end                     */
+    double warmup_cut_s;          /* CS_WL_HORIZON: warmup_fraction * t_end   */
+    const double* arrivals;       /* CS_WL_SAMPLED / CS_WL_TRACE              */
+    const double* sizes;          /* CS_WL_SAMPLED                            */
+    const int32_t* tokens_in;     /* CS_WL_TRACE                              */
+    const int32_t* tokens_out;
+    const int32_t* hop_begin;     /* CS_WL_TRACE: hops of global chain c are  */
+    const int32_t* hop_server;    /*  hop_begin[c] .. hop_begin[c+1]-1        */
+    const int32_t* hop_blocks;    /*  (server index, blocks_at_dst)           */
+    const double* server_param;   /*  4 per server: rtt+overhead ms, block
+                                      overhead ms, prefill ms, decode ms      */
+    int32_t rep_begin, n_reps, n_reps_total;
+    int64_t n_jobs;               /* n (HORIZON: the horizon_jobs cap)        */
+    int64_t warm;                 /* int(warmup_fraction*n); HORIZON: per rep */
+    double* responses;            /* as cs_jffc_sim (row o, completion order) */
+    int64_t ldr;
+    double* busy;
+    int32_t ldb;
+    cs_rep_summary* summary;
+    double* jobs;                 /* NULL or [o][n][4] job records            */
+    int64_t* rep_jobs;            /* NULL or per row o: jobs simulated (HORIZON) */
+    int32_t* rep_status;          /* per row o: CS_OK or CS_REP_*             */
+    void* queue_workspace;        /* dedicated policies: n_points*n_reps*
+                                     max_chains*queue_capacity*16 bytes      */
+    int32_t queue_capacity;       /* per chain, power of two                  */
+} cs_sim_ext_args;
+
+int cs_sim_ext(const cs_sim_ext_args* args, void* stream);
+
+/* Ragged response rows (time-horizon mode, counts[row] responses each):
+ * sums[row] = numpy pairwise sum of the row (responses.mean() numerator,
+ * sim.py:407), and entries counts[row]..ldr-1 set to +inf so cs_rep_stats
+ * can select the merged order statistics over uniform rows. */
+int cs_ragged_rows(double* d_resp, int32_t n_rows, int64_t ldr, const int64_t* d_counts,
+                   double* d_sums, void* stream);
+
 /* ------------------------------------------------------------------------ */
 /* Statistics over stored responses (run_sim aggregation, sim.py:406-438)     */
 /* ------------------------------------------------------------------------ */

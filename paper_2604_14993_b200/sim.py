@@ -7,9 +7,10 @@ exact order statistics behind the percentiles) run on the GPU through
 arrival rates) that share seed/replications in ONE call; each point's
 SimStats is identical to a separate ``run_sim`` call.
 
-Outside the hot path and raising
-NotImplementedError: dedicated-queue policies (jsq/jiq/sed/sa-jsq), sampled
-and trace workloads, and the time-horizon mode.
+The rest of the signature (dedicated-queue
+policies jsq/sa-jsq/jiq/sed, sampled and trace workloads, the time-horizon
+mode) runs through ``sim_ext.simulate_ext`` (csrc/sim_ext.cu), also on the
+GPU and bit-exact.
 """
 
 from __future__ import annotations
@@ -195,14 +196,12 @@ def _ci_half_width(values) -> float:
 
 
 def _require_supported(cfg: SimConfig) -> None:
-    if cfg.policy != "jffc":
-        raise NotImplementedError(
-            f"policy {cfg.policy!r}: dedicated-queue baselines are a later-round GPU path "
-            "(SURVEY.md §8(f) row 2); the engine simulates 'jffc'")
-    if not isinstance(cfg.workload, PoissonWorkload):
-        raise NotImplementedError("sampled/trace workloads are SURVEY.md §8(f) row 3")
-    if cfg.horizon_time_s is not None:
-        raise NotImplementedError("time-horizon mode is SURVEY.md §8(f) row 4")
+    """The fast batched path: JFFC over a Poisson stream without time horizon."""
+    from .sim_ext import needs_ext
+
+    if needs_ext(cfg):
+        raise ValueError("run_sim_batch: batched sweeps cover jffc/Poisson configs; "
+                         "use run_sim for other policies and workloads")
 
 
 def _stats_from(cfg: SimConfig, summ: np.ndarray, busy: np.ndarray, order_stats: dict,
@@ -236,7 +235,10 @@ def _stats_from(cfg: SimConfig, summ: np.ndarray, busy: np.ndarray, order_stats:
     if cfg.collect_jobs and jobs is not None:
         records = tuple((r, float(a), float(s), float(f), int(k))
                         for r in range(R) for a, s, f, k in jobs[r])
-    offered = cfg.workload.rate
+    # sim.py:442,452: offered load is the Poisson rate, else the measured one
+    offered = cfg.workload.rate if isinstance(cfg.workload, PoissonWorkload) or (
+        hasattr(cfg.workload, "rate") and not hasattr(cfg.workload, "sizes")) else lam_eff
+    unstable = bool(offered >= cfg.total_rate) if not math.isnan(offered) else False
     return SimStats(
         policy=cfg.policy, jobs_counted=counted, mean_response_s=mean_resp,
         median_response_s=qv[0.5], p95_response_s=qv[0.95], p99_response_s=qv[0.99],
@@ -244,7 +246,7 @@ def _stats_from(cfg: SimConfig, summ: np.ndarray, busy: np.ndarray, order_stats:
         mean_occupancy=mean_occ, response_ci_half_width_s=_ci_half_width(rep_means),
         occupancy_ci_half_width=_ci_half_width(rep_occ), per_chain_utilization=util,
         lambda_effective=lam_eff, little_law_gap=little,
-        unstable=bool(offered >= cfg.total_rate), seed=cfg.seed, replications=R,
+        unstable=unstable, seed=cfg.seed, replications=R,
         rep_mean_response_s=rep_means, rep_mean_occupancy=rep_occ,
         occ_first_half=_nanmean([float(x) for x in summ["occ_first_half"]]),
         occ_second_half=_nanmean([float(x) for x in summ["occ_second_half"]]),
@@ -334,4 +336,9 @@ def run_sim(config: SimConfig) -> SimStats:
 
     ``workers`` is accepted for signature parity; parallelism is the GPU's.
     """
+    from .sim_ext import needs_ext, simulate_ext
+
+    if needs_ext(config):
+        summ, busy, os_, jobs, _ = simulate_ext(config)
+        return _stats_from(config, summ, busy, os_, jobs)
     return run_sim_batch([config])[0]

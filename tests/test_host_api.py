@@ -87,10 +87,18 @@ def test_simconfig_validation():
     dict(workload=P.SampledWorkload((0.0,), (1.0,))),
     dict(horizon_time_s=10.0),
 ])
-def test_unsupported_modes_raise_not_implemented(kw):
+def test_extended_modes_have_no_cpu_path(kw):
+    """Policies / sampled / horizon run on the GPU (sim_ext.cu) or not at all:
+    without a device the call fails loudly, and the batched jffc sweep API
+    rejects them."""
+    import torch
+
     cfg = P.SimConfig(**{**dict(rates=(1.0,), capacities=(1,), workload=P.PoissonWorkload(0.5)), **kw})
-    with pytest.raises(NotImplementedError):
-        P.run_sim(cfg)
+    if not torch.cuda.is_available():
+        with pytest.raises(P.NativeUnavailable):
+            P.run_sim(cfg)
+    with pytest.raises(ValueError, match="run_sim_batch"):
+        P.run_sim_batch([cfg])
 
 
 @pytest.mark.parametrize("n", [1, 2, 7, 100, 1001, 90000, 123457])
