@@ -68,7 +68,7 @@ EXPORTS = (
     "cs_philox_keys", "cs_exp_streams", "cs_jffc_sim", "cs_jffc_sim_workspace_bytes",
     "cs_rep_stats", "cs_rep_stats_dist", "cs_run_sim_host", "cs_gbp_batch", "cs_gca_batch",
     "cs_nccl_unique_id", "cs_comm_init", "cs_comm_destroy", "cs_occupancy_bounds",
-    "cs_birth_death_occupancy",
+    "cs_birth_death_occupancy", "cs_sim_ext", "cs_ragged_rows",
 )
 
 _lib = None
@@ -113,6 +113,8 @@ def load(require_device: bool = True):
             [C.c_int32, C.c_int32] + [vp] * 7 + [vp]
         L.cs_occupancy_bounds.argtypes = [vp, C.c_int32, vp, vp, C.c_int32, vp, vp, vp]
         L.cs_birth_death_occupancy.argtypes = [vp, C.c_int32, vp, C.c_int32, vp, vp, vp]
+        L.cs_sim_ext.argtypes = [vp, vp]
+        L.cs_ragged_rows.argtypes = [vp, C.c_int32, C.c_int64, vp, vp, vp]
         _lib = L
     if require_device and _lib.cs_device_count() == 0:
         raise NativeUnavailable("no CUDA device visible: the chainserve B200 engine has no CPU path")

@@ -459,27 +459,53 @@ __global__ void __launch_bounds__(32 * EXT_WARPS) sim_ext_kernel(const cs_sim_ex
 // numpy pairwise_sum (loops_utils.h.src) of a[0:n]: leaves of <= 128 values
 // (8 accumulators, ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), then the remainder;
 // < 8 values: 0.0 + sequential), split at n/2 rounded down to a multiple of 8.
-__device__ double np_pairwise(const double* a, int64_t n) {
-    if (n <= 128) {
-        if (n < 8) {
-            double res = 0.0;
-            for (int64_t i = 0; i < n; i++) res = __dadd_rn(res, a[i]);
-            return res;
-        }
-        double r[8];
-        for (int q = 0; q < 8; q++) r[q] = a[q];
-        int64_t i = 8;
-        for (; i < n - n % 8; i += 8)
-            for (int q = 0; q < 8; q++) r[q] = __dadd_rn(r[q], a[i + q]);
-        double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
-                               __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-        for (; i < n; i++) res = __dadd_rn(res, a[i]);
+__device__ double np_leaf(const double* a, int64_t n) {
+    if (n < 8) {
+        double res = 0.0;
+        for (int64_t i = 0; i < n; i++) res = __dadd_rn(res, a[i]);
         return res;
     }
-    int64_t n2 = n / 2;
-    n2 -= n2 % 8;
-    const double left = np_pairwise(a, n2);
-    return __dadd_rn(left, np_pairwise(a + n2, n - n2));
+    double r[8];
+    for (int q = 0; q < 8; q++) r[q] = a[q];
+    int64_t i = 8;
+    for (; i < n - n % 8; i += 8)
+        for (int q = 0; q < 8; q++) r[q] = __dadd_rn(r[q], a[i + q]);
+    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+    for (; i < n; i++) res = __dadd_rn(res, a[i]);
+    return res;
+}
+
+// the recursion unrolled onto explicit stacks (device recursion would need
+// a dynamic call stack): tasks are "evaluate [off, off+n)" or "combine the
+// two values on top"; depth <= 3 per level, <= 40 levels for n < 2^46
+__device__ double np_pairwise(const double* a, int64_t n) {
+    int64_t t_off[128], t_n[128];  // t_n < 0: combine task
+    double vals[64];
+    int ts = 0, vs = 0;
+    t_off[ts] = 0;
+    t_n[ts++] = n;
+    while (ts > 0) {
+        ts--;
+        const int64_t off = t_off[ts], m = t_n[ts];
+        if (m < 0) {
+            const double b = vals[--vs];
+            const double l = vals[--vs];
+            vals[vs++] = __dadd_rn(l, b);
+        } else if (m <= 128) {
+            vals[vs++] = np_leaf(a + off, m);
+        } else {
+            int64_t m2 = m / 2;
+            m2 -= m2 % 8;
+            t_off[ts] = 0;
+            t_n[ts++] = -1;  // combine after both halves
+            t_off[ts] = off + m2;
+            t_n[ts++] = m - m2;
+            t_off[ts] = off;
+            t_n[ts++] = m2;  // left half first
+        }
+    }
+    return vals[0];
 }
 
 // Ragged response rows (time-horizon mode: each replication simulates its
