@@ -391,6 +391,194 @@ int orc_simulate_once(int K, const double* rates, const int32_t* caps, double la
     return ORC_OK;
 }
 
+/* ======================================================================== */
+/* _simulate_once with explicit inputs (sim.py:181-324, every policy):       */
+/* arrivals[n] and per-(job, chain) durations come from the caller, who      */
+/* restates _materialize / duration() (sim.py:136-178,199-203) in numpy.     */
+/* dur: size-based when dur_kn == NULL (d = sizes[j] * (1.0/rates[k])), else */
+/* dur_kn[j*K + k] (trace workloads).  policy: 0 jffc (central FIFO queue),  */
+/* 1 jsq, 2 sa-jsq, 3 jiq, 4 sed (policy_step, sim.py:75-117; one FIFO per   */
+/* chain).  Same outputs as orc_simulate_once.                               */
+/* ======================================================================== */
+static int policy_arrival(int policy, int K, const double* rates, const int32_t* caps,
+                          const int32_t* z, const int64_t* qlen) {
+    if (policy == 0) {
+        for (int k = 0; k < K; k++)
+            if (z[k] < caps[k]) return k;
+        return -1;
+    }
+    int best = 0;
+    if (policy == 4) { /* sed: min ((totals+1)/rates[k], k) */
+        double bv = 0.0;
+        for (int k = 0; k < K; k++) {
+            double v = (double)(z[k] + qlen[k] + 1) / rates[k];
+            if (k == 0 || v < bv) {
+                bv = v;
+                best = k;
+            }
+        }
+        return best;
+    }
+    if (policy == 3) /* jiq: first idle (totals < caps), else jsq */
+        for (int k = 0; k < K; k++)
+            if (z[k] + qlen[k] < caps[k]) return k;
+    int64_t bt = 0; /* jsq / sa-jsq: min (totals, k) */
+    for (int k = 0; k < K; k++) {
+        int64_t tot = z[k] + qlen[k];
+        if (k == 0 || tot < bt) {
+            bt = tot;
+            best = k;
+        }
+    }
+    return best;
+}
+
+int orc_simulate_ext(int K, const double* rates, const int32_t* caps, int policy, int64_t n,
+                     int64_t warm, const double* arr, const double* sizes, const double* dur_kn,
+                     double* responses, double* busy_out, double* jobs, orc_rep_summary* out) {
+    if (K < 1 || n < 1 || warm < 0 || warm >= n || policy < 0 || policy > 4) return ORC_INVALID;
+    double* start_t = (double*)malloc(sizeof(double) * n);
+    int32_t* z = (int32_t*)calloc(K, sizeof(int32_t));
+    double* busy = (double*)calloc(K, sizeof(double));
+    double* inv_mu = (double*)malloc(sizeof(double) * K);
+    int64_t cap_total = 0;
+    for (int k = 0; k < K; k++) cap_total += caps[k];
+    ev* heap = (ev*)malloc(sizeof(ev) * (cap_total + 1));
+    /* queues: central (policy 0) or one per chain; each a FIFO of job ids,
+     * stored as a chain-tagged array with per-chain linked order */
+    int64_t* qnext = (int64_t*)malloc(sizeof(int64_t) * n);  /* next job of the same queue */
+    int nq = policy == 0 ? 1 : K;
+    int64_t* qhead = (int64_t*)malloc(sizeof(int64_t) * nq);
+    int64_t* qtail = (int64_t*)malloc(sizeof(int64_t) * nq);
+    int64_t* qlen = (int64_t*)calloc(K, sizeof(int64_t));
+    if (!start_t || !z || !busy || !inv_mu || !heap || !qnext || !qhead || !qtail || !qlen) {
+        free(start_t); free(z); free(busy); free(inv_mu); free(heap); free(qnext);
+        free(qhead); free(qtail); free(qlen);
+        return ORC_INTERNAL;
+    }
+    for (int q = 0; q < nq; q++) qhead[q] = qtail[q] = -1;
+    for (int k = 0; k < K; k++) inv_mu[k] = 1.0 / rates[k];
+    int64_t mid = warm + (n - warm) / 2;
+    int64_t hn = 0, n_sys = 0, n_resp = 0, end_queue = 0, qtot = 0;
+    int started = 0;
+    double last_t = 0.0, area = 0.0, w_start = NAN;
+    double t_mid = NAN, area_mid = NAN, t_end = NAN, area_end = NAN;
+    double wait_sum = 0.0, service_sum = 0.0;
+
+#define ADV(T)                                                                 \
+    do {                                                                       \
+        double dt_ = (T) - last_t;                                             \
+        if (dt_ > 0.0) {                                                       \
+            area += (double)n_sys * dt_;                                       \
+            for (int k_ = 0; k_ < K; k_++) busy[k_] += (double)z[k_] * dt_;    \
+            last_t = (T);                                                      \
+        }                                                                      \
+    } while (0)
+#define START(J, KK, T)                                                        \
+    do {                                                                       \
+        z[KK] += 1;                                                            \
+        double d_ = dur_kn ? dur_kn[(J) * K + (KK)] : sizes[J] * inv_mu[KK];   \
+        start_t[J] = (T);                                                      \
+        if ((J) >= warm) {                                                     \
+            wait_sum += (T) - arr[J];                                          \
+            service_sum += d_;                                                 \
+        }                                                                      \
+        ev e_ = {(T) + d_, (KK), (J)};                                         \
+        heap_push(heap, &hn, e_);                                              \
+    } while (0)
+
+    int64_t i = 0;
+    while (i < n || hn > 0) {
+        double t_arr = i < n ? arr[i] : INFINITY;
+        if (hn > 0 && heap[0].finish <= t_arr) {
+            ev e = heap_pop(heap, &hn);
+            double t = e.finish;
+            ADV(t);
+            z[e.k] -= 1;
+            n_sys -= 1;
+            if (e.j >= warm) responses[n_resp++] = t - arr[e.j];
+            if (jobs) {
+                jobs[4 * e.j + 0] = arr[e.j];
+                jobs[4 * e.j + 1] = start_t[e.j];
+                jobs[4 * e.j + 2] = t;
+                jobs[4 * e.j + 3] = (double)e.k;
+            }
+            int q = policy == 0 ? 0 : e.k;
+            if (qhead[q] >= 0) {
+                int64_t jj = qhead[q];
+                qhead[q] = qnext[jj];
+                if (qhead[q] < 0) qtail[q] = -1;
+                if (policy != 0) qlen[q]--;
+                qtot--;
+                START(jj, e.k, t);
+            }
+            continue;
+        }
+        double t = t_arr;
+        ADV(t);
+        if (i == warm && !started) {
+            started = 1;
+            w_start = t;
+            last_t = t;
+            area = 0.0;
+            for (int k = 0; k < K; k++) busy[k] = 0.0;
+        }
+        n_sys += 1;
+        int target = policy_arrival(policy, K, rates, caps, z, qlen);
+        int q = -1;
+        if (policy == 0) {
+            if (target < 0) q = 0;
+        } else if (z[target] >= caps[target]) {
+            q = target;
+        }
+        if (q < 0) {
+            START(i, target, t);
+        } else {
+            qnext[i] = -1;
+            if (qtail[q] >= 0) qnext[qtail[q]] = i; else qhead[q] = i;
+            qtail[q] = i;
+            if (policy != 0) qlen[q]++;
+            qtot++;
+        }
+        if (i == mid) {
+            t_mid = t;
+            area_mid = area;
+        }
+        if (i == n - 1) {
+            t_end = t;
+            area_end = area;
+            for (int k = 0; k < K; k++) busy_out[k] = busy[k];
+            end_queue = qtot;
+        }
+        i++;
+    }
+#undef ADV
+#undef START
+    double window = t_end - w_start;
+    out->wait_sum = wait_sum;
+    out->service_sum = service_sum;
+    out->counted = n_resp;
+    out->window_s = window;
+    if (window > 0) {
+        out->mean_occupancy = area_end / window;
+        out->lambda_effective = (double)(n - warm) / window;
+    } else {
+        out->mean_occupancy = NAN;
+        out->lambda_effective = NAN;
+    }
+    out->occ_first_half = t_mid > w_start ? area_mid / (t_mid - w_start) : NAN;
+    out->occ_second_half = t_end > t_mid ? (area_end - area_mid) / (t_end - t_mid) : NAN;
+    out->end_queue_len = end_queue;
+    out->w_start = w_start;
+    out->t_mid = t_mid;
+    out->area_mid = area_mid;
+    out->t_end = t_end;
+    out->area_end = area_end;
+    free(start_t); free(z); free(busy); free(inv_mu); free(heap); free(qnext);
+    free(qhead); free(qtail); free(qlen);
+    return ORC_OK;
+}
+
 typedef struct {
     int K;
     const double* rates;

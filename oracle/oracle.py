@@ -73,6 +73,10 @@ def lib():
             C.c_int64, C.c_int64, P(C.c_int32), P(C.c_int32), P(C.c_int64), C.c_int32,
             C.c_int32, P(C.c_int32), P(C.c_int32), P(C.c_int32), P(C.c_double),
             P(C.c_int32), P(C.c_int64)]
+        L.orc_simulate_ext.argtypes = [
+            C.c_int, P(C.c_double), P(C.c_int32), C.c_int, C.c_int64, C.c_int64, P(C.c_double),
+            P(C.c_double), P(C.c_double), P(C.c_double), P(C.c_double), P(C.c_double),
+            P(RepSummary)]
         _lib = L
     return _lib
 
@@ -123,6 +127,80 @@ def simulate_once(rates, caps, lam, n, warmup_fraction, seed, rep, collect_jobs=
         _p(jobs, C.c_double) if jobs is not None else None, C.byref(s))
     if st != OK:
         raise RuntimeError(f"oracle simulate_once status {st}")
+    out = {f: getattr(s, f) for f, _ in RepSummary._fields_}
+    out["responses"] = resp[: s.counted].copy()
+    out["busy_time_s"] = busy
+    out["jobs"] = jobs
+    return out
+
+
+POLICY_CODE = {"jffc": 0, "jsq": 1, "sa-jsq": 2, "jiq": 3, "sed": 4}
+HBLK = 4096
+
+
+def poisson_inputs(lam, n, seed, rep, horizon=None):
+    """_materialize, Poisson branch (sim.py:136-160): (arrivals, sizes).
+    Without a horizon: cumsum(exponential(1/lam, n)); with one: 4096-draw
+    blocks cumsum(block) + total while total < t_end and fewer than n drawn,
+    then arrivals <= t_end, at most n; sizes drawn after every block."""
+    key = philox_key(seed, rep)
+    scale = 1.0 / lam
+    if horizon is None:
+        S, _ = standard_exponential(key, 2 * n)
+        return np.cumsum(scale * S[:n]), 1.0 * S[n:]
+    S, _ = standard_exponential(key, HBLK * (-(-n // HBLK)) + n)
+    chunks, total, count, pos = [], 0.0, 0, 0
+    while total < horizon and count < n:
+        block = np.cumsum(scale * S[pos:pos + HBLK]) + total
+        pos += HBLK
+        chunks.append(block)
+        total = block[-1]
+        count += block.size
+    arrivals = np.concatenate(chunks)
+    arrivals = arrivals[arrivals <= horizon][:n]
+    return arrivals, 1.0 * S[pos:pos + arrivals.size]
+
+
+def trace_durations(tin, tout, chains_hops, server_params):
+    """ServiceTimeModel.request_service_time (workload.py:150-164) for every
+    (job, chain): chains_hops[k] = [(server, blocks_at_dst), ...] (tail hop
+    excluded); server_params[s] = (rtt+overhead ms, block overhead ms,
+    prefill ms, decode ms).  Returns an [n, K] array."""
+    tin = np.asarray(tin, np.float64)
+    tout_i = np.asarray(tout, np.int64)
+    tout = tout_i.astype(np.float64)
+    out = np.empty((tin.size, len(chains_hops)))
+    for k, hops in enumerate(chains_hops):
+        total = np.zeros(tin.size)
+        for s, m in hops:
+            ptm, ovh, pre, dec = server_params[s]
+            total = total + tout * ptm / 1000.0
+            total = total + ((ovh + pre * tin) + dec * (tout_i - 1).astype(np.float64)) / 1000.0 * m
+        out[:, k] = total
+    return out
+
+
+def simulate_ext(rates, caps, policy, arrivals, warm, sizes=None, durations=None,
+                 collect_jobs=False):
+    """sim.py:_simulate_once on explicit inputs, any policy.  Returns a dict
+    of RepResult fields (as simulate_once)."""
+    rates = np.ascontiguousarray(rates, np.float64)
+    caps = np.ascontiguousarray(caps, np.int32)
+    arr = np.ascontiguousarray(arrivals, np.float64)
+    K, n = len(rates), arr.size
+    sz = None if sizes is None else np.ascontiguousarray(sizes, np.float64)
+    dur = None if durations is None else np.ascontiguousarray(durations, np.float64)
+    resp = np.empty(max(n - warm, 1), np.float64)
+    busy = np.empty(K, np.float64)
+    jobs = np.empty((n, 4), np.float64) if collect_jobs else None
+    s = RepSummary()
+    st = lib().orc_simulate_ext(
+        K, _p(rates, C.c_double), _p(caps, C.c_int32), POLICY_CODE[policy], n, warm,
+        _p(arr, C.c_double), _p(sz, C.c_double) if sz is not None else None,
+        _p(dur, C.c_double) if dur is not None else None, _p(resp, C.c_double),
+        _p(busy, C.c_double), _p(jobs, C.c_double) if jobs is not None else None, C.byref(s))
+    if st != OK:
+        raise RuntimeError(f"oracle simulate_ext status {st}")
     out = {f: getattr(s, f) for f, _ in RepSummary._fields_}
     out["responses"] = resp[: s.counted].copy()
     out["busy_time_s"] = busy

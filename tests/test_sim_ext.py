@@ -121,3 +121,48 @@ def test_run_sim_ext_matches_reference(gx, i):
             assert same_float(g, v), (k, g, v)
         else:
             assert g == v, (k, g, v)
+
+
+def _random_system(rng, K, C):
+    rates = tuple(sorted((float(x) for x in rng.uniform(0.2, 2.0, K)), reverse=True))
+    caps = [1] * K
+    for _ in range(C - K):
+        caps[int(rng.integers(K))] += 1
+    return rates, tuple(caps)
+
+
+EXT_RANDOM = [(K, C, pol, rho, hz) for (K, C) in ((1, 3), (3, 9), (12, 40), (40, 100))
+              for pol in ("jffc", "jsq", "jiq", "sed") for rho, hz in ((0.6, None), (0.97, None),
+                                                                       (1.2, 2500.0))]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("K,C,pol,rho,hz", EXT_RANDOM)
+def test_simulate_ext_matches_oracle(oracle, K, C, pol, rho, hz):
+    """Fresh seeded configurations beyond the golden ones (K up to 40 chains,
+    overloaded systems with long dedicated queues, time horizon): GPU vs the
+    pinned oracle, bit-exact."""
+    import paper_2604_14993_b200 as P
+    from conftest import ext_inputs
+    from paper_2604_14993_b200.sim_ext import simulate_ext
+
+    rng = np.random.default_rng(K * 7919 + C)
+    rates, caps = _random_system(rng, K, C)
+    nu = sum(r * c for r, c in zip(rates, caps))
+    lam = rho * nu
+    n, wf, seed, R = 4000, 0.1, 17, 3
+    t_end = None if hz is None else hz / lam
+    cfg = P.SimConfig(rates=rates, capacities=caps, workload=P.PoissonWorkload(lam), policy=pol,
+                      horizon_jobs=n, horizon_time_s=t_end, warmup_fraction=wf, seed=seed,
+                      replications=R, collect_jobs=True)
+    summ, busy, _, jobs, resp = simulate_ext(cfg, return_responses=True, queue_capacity=64)
+    c = {"workload": {"kind": "poisson", "lam": lam}, "n": n, "wf": wf, "horizon": t_end,
+         "seed": seed}
+    for r in range(R):
+        arr, warm, sizes, _ = ext_inputs(oracle, c, {}, r)
+        o = oracle.simulate_ext(rates, caps, pol, arr, warm, sizes, None, collect_jobs=True)
+        assert np.array_equal(bits(resp[r]), bits(o["responses"])), r
+        assert np.array_equal(bits(busy[r]), bits(o["busy_time_s"])), r
+        assert np.array_equal(bits(jobs[r]), bits(o["jobs"])), r
+        for f in FIELDS:
+            assert same_float(summ[r][f], o[f]), (r, f)
