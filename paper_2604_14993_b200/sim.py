@@ -208,6 +208,8 @@ def _stats_from(cfg: SimConfig, summ: np.ndarray, busy: np.ndarray, order_stats:
                 jobs: np.ndarray | None) -> SimStats:
     """sim.py:406-456 on per-replication summaries (no response re-reads on host)."""
     R = cfg.replications
+    if np.any(summ["counted"] < 0):  # jffc_sim_k1_kernel merge-feed overflow (never seen)
+        raise AssertionError("simulation merge feed overflowed (exact finish-time ties)")
     counted = int(sum(int(c) for c in summ["counted"]))
     rep_means = tuple(float(x) for x in summ["resp_mean"])
     rep_occ = tuple(float(x) for x in summ["mean_occupancy"])
