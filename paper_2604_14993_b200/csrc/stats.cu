@@ -151,7 +151,7 @@ __global__ void compact_bucket_kernel(const double* __restrict__ resp, int64_t n
 template <int NB>
 struct Brackets {
     uint64_t lo[NB], hi[NB];
-    uint32_t lo_hw[NB], hi_hw[NB];
+    uint32_t lo_hw[NB], hi_hw[NB], wid_hw[NB];
     uint32_t cnt[NB];
 };
 
@@ -210,6 +210,7 @@ __global__ void __launch_bounds__(LB_WARPS * 32) row_stats_kernel(
             br.hi[q] = q < nl ? hi[g * MAX_LISTS + q] : 0ull;
             br.lo_hw[q] = (uint32_t)(br.lo[q] >> 32);
             br.hi_hw[q] = (uint32_t)(br.hi[q] >> 32);
+            br.wid_hw[q] = q < nl ? br.hi_hw[q] - br.lo_hw[q] : 0u;
             br.cnt[q] = 0;
         }
         int sp = 0;
@@ -247,25 +248,38 @@ __global__ void __launch_bounds__(LB_WARPS * 32) row_stats_kernel(
             for (int t = 1; t < 16; t++)
                 if (j + 8 * t < main_end) acc = __dadd_rn(acc, v[t]);
             if (do_bracket) {
-                uint32_t hit = 0;     // bit t: value t falls inside a bracket
-                uint64_t which = 0;   // its bracket slot, 4 bits per value
+                // fast path on the high words: "below bracket q" is exact
+                // unless hw == lo_hw[q]; anything within a bracket's
+                // high-word span is flagged for the exact path
+                uint32_t nearm = 0;
 #pragma unroll
                 for (int t = 0; t < 16; t++) {
-                    const int q = classify_one<NB>(br, dbits(v[t]), j + 8 * t < main_end);
-                    if (q >= 0) {
-                        hit |= 1u << t;
-                        which |= (uint64_t)q << (4 * t);
+                    const uint32_t hw = (uint32_t)(dbits(v[t]) >> 32);
+                    const bool have = j + 8 * t < main_end;
+                    bool nr = false;
+#pragma unroll
+                    for (int q = 0; q < NB; q++) {
+                        br.cnt[q] += (have && hw < br.lo_hw[q]) ? 1u : 0u;
+                        nr |= hw - br.lo_hw[q] <= br.wid_hw[q];
                     }
+                    nearm |= (have && nr) ? (1u << t) : 0u;
                 }
-                // the rare candidates: one vote per 16 values, re-read from L1
-                while (__any_sync(0xffffffffu, hit != 0)) {
+                // the rare near values: exact 64-bit classification (re-read
+                // from L1), count fix-up and candidate append
+                while (__any_sync(0xffffffffu, nearm != 0)) {
                     int list = -1;
                     double w = 0.0;
-                    if (hit) {
-                        const int t = __ffs(hit) - 1;
-                        hit &= hit - 1;
+                    if (nearm) {
+                        const int t = __ffs(nearm) - 1;
+                        nearm &= nearm - 1;
                         w = __ldg(a + j + 8 * t);
-                        list = (int)(g * MAX_LISTS + ((which >> (4 * t)) & 15));
+                        const uint64_t u = dbits(w);
+                        const uint32_t hw = (uint32_t)(u >> 32);
+#pragma unroll
+                        for (int q = 0; q < NB; q++) {
+                            br.cnt[q] += (hw == br.lo_hw[q] && u < br.lo[q]) ? 1u : 0u;
+                            if (u >= br.lo[q] && u <= br.hi[q]) list = (int)(g * MAX_LISTS + q);
+                        }
                     }
                     append(list, w, fill, off, cap, cand);
                 }
