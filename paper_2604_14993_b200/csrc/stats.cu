@@ -30,6 +30,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <utility>
 #include <vector>
 
 #include "cs_internal.cuh"
@@ -178,10 +179,10 @@ __device__ __forceinline__ int classify_one(Brackets<NB>& br, uint64_t u, bool h
 
 // The one full pass, one warp per replication row: numpy pairwise leaf sums
 // (8 lanes per leaf, 4 leaves at a time; a leaf's values are loaded up front
-// for memory-level parallelism), the split tree evaluated in order with a
-// small stack (after leaf i, merges[i] internal nodes complete), and the
-// optional bracket counting/compaction.  The plan (leaf offset, length,
-// merges) sits in shared memory.
+// for memory-level parallelism) into a per-warp shared-memory array, the
+// split tree combined height by height with the lanes in parallel, and the
+// optional bracket counting/compaction.  The plan (leaf offsets, lengths,
+// height-ordered nodes) sits in shared memory.
 constexpr int LB_WARPS = 8;
 
 template <int NB>
@@ -191,15 +192,22 @@ __global__ void __launch_bounds__(LB_WARPS * 32) row_stats_kernel(
     double* __restrict__ row_sums, int do_bracket, const int32_t* __restrict__ grp_nlist,
     const uint64_t* __restrict__ lo, const uint64_t* __restrict__ hi, const int64_t* __restrict__ off,
     const int64_t* __restrict__ cap, unsigned long long* __restrict__ fill,
-    unsigned long long* __restrict__ below, double* __restrict__ cand) {
-    extern __shared__ int32_t plan[];  // [3][L]: offset, length, merges
-    for (int q = threadIdx.x; q < 3 * L; q += blockDim.x) plan[q] = g_plan[q];
+    unsigned long long* __restrict__ below, double* __restrict__ cand, int32_t n_heights) {
+    // shared: per-warp leaf values [LB_WARPS][L] doubles, then the plan:
+    // leaf offset[L], leaf length[L], height offsets[n_heights + 1] and the
+    // internal nodes in height order as (a, b) pairs: v[a] = v[a] + v[b]
+    // (a = the node's leftmost leaf, b = its right child's leftmost leaf)
+    extern __shared__ double row_sh[];
+    int32_t* plan = reinterpret_cast<int32_t*>(row_sh + (size_t)LB_WARPS * L);
+    const int plan_words = 2 * L + (n_heights + 1) + 2 * (L - 1);
+    for (int q = threadIdx.x; q < plan_words; q += blockDim.x) plan[q] = g_plan[q];
     __syncthreads();
     const int32_t* leaf_off = plan;
     const int32_t* leaf_len = plan + L;
-    const int32_t* leaf_mrg = plan + 2 * L;
+    const int32_t* h_off = plan + 2 * L;
+    const int32_t* nodes = h_off + n_heights + 1;
+    double* lv = row_sh + (size_t)(threadIdx.x >> 5) * L;
     const int lane = threadIdx.x & 31, j = lane & 7, sub = lane >> 3, warp = threadIdx.x >> 5;
-    double stk[48];  // lane 0's split-tree stack (depth <= log2(m/64) + 2)
     for (int64_t row = (int64_t)blockIdx.x * LB_WARPS + warp; row < n_rows; row += (int64_t)gridDim.x * LB_WARPS) {
         const int64_t g = row / rows_per_group;
         const int nl = do_bracket ? grp_nlist[g] : 0;  // warp-uniform, <= NB (checked on the host)
@@ -213,10 +221,9 @@ __global__ void __launch_bounds__(LB_WARPS * 32) row_stats_kernel(
             br.wid_hw[q] = q < nl ? br.hi_hw[q] - br.lo_hw[q] : 0u;
             br.cnt[q] = 0;
         }
-        int sp = 0;
         const double* __restrict__ rowp = resp + row * ldr;
         // software pipeline: the next leaf group's loads are in flight while
-        // this group's split-tree merges run
+        // this group's values are classified and summed
         double nv[16];
         {
             const int leaf = sub;
@@ -302,23 +309,20 @@ __global__ void __launch_bounds__(LB_WARPS * 32) row_stats_kernel(
                     append(q >= 0 ? (int)(g * MAX_LISTS + q) : -1, w, fill, off, cap, cand);
                 }
             }
-            // leaves l0..l0+3 (lanes 0, 8, 16, 24) into lane 0's stack, in order
-            const double r1 = __shfl_sync(0xffffffffu, res, 8);
-            const double r2 = __shfl_sync(0xffffffffu, res, 16);
-            const double r3 = __shfl_sync(0xffffffffu, res, 24);
-            if (lane == 0) {
-                const double rs[4] = {res, r1, r2, r3};
-                for (int q = 0; q < 4 && l0 + q < L; q++) {
-                    stk[sp++] = rs[q];
-                    for (int k = leaf_mrg[l0 + q]; k > 0; k--) {
-                        const double b = stk[--sp];
-                        stk[sp - 1] = __dadd_rn(stk[sp - 1], b);
-                    }
-                }
+            if (j == 0 && valid) lv[leaf] = res;  // leaves l0..l0+3 (lanes 0, 8, 16, 24)
+        }
+        // the split tree, one height at a time: nodes of equal height have
+        // disjoint subtrees, so the lanes combine them in parallel
+        __syncwarp();
+        for (int h = 0; h < n_heights; h++) {
+            for (int i = h_off[h] + lane; i < h_off[h + 1]; i += 32) {
+                const int na = nodes[2 * i], nb = nodes[2 * i + 1];
+                lv[na] = __dadd_rn(lv[na], lv[nb]);
             }
+            __syncwarp();
         }
         if (lane == 0) {
-            const double total = sp > 0 ? stk[0] : 0.0;
+            const double total = L > 0 ? lv[0] : 0.0;
             if (row_sums) row_sums[row] = total;
             if (summ) {
                 summ[row].resp_sum = total;
@@ -550,25 +554,31 @@ static int select_rows(const double* d_resp, int64_t n_groups, int64_t rows_per_
 }
 
 // Split tree of numpy's pairwise sum for rows of m values (cached per m):
-// leaves in order and, per leaf, the number of internal nodes that complete
-// right after it (the in-order evaluation schedule of the recursion).
+// leaves in order, and the internal nodes grouped by height (leaves 0): a
+// node stores its value in its leftmost leaf's slot, so combining it is
+// v[a] = v[a] + v[b] with a = its leftmost leaf, b = its right child's.
 struct PairwisePlan {
     int64_t m = -1;
-    std::vector<int32_t> leaf_off, leaf_len, merges;
+    std::vector<int32_t> leaf_off, leaf_len;
+    std::vector<std::vector<int32_t>> by_height;  // (a, b) pairs per height - 1
 };
 
-static void plan_build(PairwisePlan& pl, int64_t off, int64_t n) {
+// returns (height, leftmost leaf) of the subtree over [off, off + n)
+static std::pair<int, int32_t> plan_build(PairwisePlan& pl, int64_t off, int64_t n) {
     if (n <= 128) {
         pl.leaf_off.push_back((int32_t)off);
         pl.leaf_len.push_back((int32_t)n);
-        pl.merges.push_back(0);
-        return;
+        return {0, (int32_t)pl.leaf_off.size() - 1};
     }
     int64_t n2 = n / 2;
     n2 -= n2 % 8;
-    plan_build(pl, off, n2);
-    plan_build(pl, off + n2, n - n2);
-    pl.merges.back() += 1;  // this node completes right after its last leaf
+    const auto l = plan_build(pl, off, n2);
+    const auto r = plan_build(pl, off + n2, n - n2);
+    const int h = std::max(l.first, r.first) + 1;
+    if ((int)pl.by_height.size() < h) pl.by_height.resize(h);
+    pl.by_height[h - 1].push_back(l.second);
+    pl.by_height[h - 1].push_back(r.second);
+    return {h, l.second};
 }
 
 static const PairwisePlan& pairwise_plan(int64_t m) {
@@ -613,22 +623,30 @@ extern "C" int cs_rep_stats_impl(const double* d_resp, int32_t n_groups, int64_t
         target[i] = k;
     }
     int rc;
-    // ---- pairwise plan (leaf offsets, lengths, merge schedule) ----
+    // ---- pairwise plan (leaf offsets, lengths, height-ordered nodes) ----
     const PairwisePlan& pl = pairwise_plan(m);
     const int32_t L = (int32_t)pl.leaf_off.size();
-    const size_t smem = sizeof(int32_t) * 3 * (size_t)L;
+    const int32_t n_heights = (int32_t)pl.by_height.size();
+    const size_t plan_words = 2 * (size_t)L + n_heights + 1 + 2 * (size_t)std::max(L - 1, 0);
+    const size_t smem = sizeof(double) * LB_WARPS * (size_t)L + sizeof(int32_t) * plan_words;
     if (smem > 200 * 1024) {
         set_error("cs_rep_stats: rows of %lld responses exceed the on-chip pairwise plan", (long long)m);
         return CS_UNSUPPORTED;
     }
     DBuf b_plan;
-    if ((rc = b_plan.alloc(std::max<size_t>(smem, 16), st))) return rc;
+    if ((rc = b_plan.alloc(std::max<size_t>(sizeof(int32_t) * plan_words, 16), st))) return rc;
     {
-        std::vector<int32_t> h(3 * (size_t)L);
-        std::copy(pl.leaf_off.begin(), pl.leaf_off.end(), h.begin());
-        std::copy(pl.leaf_len.begin(), pl.leaf_len.end(), h.begin() + L);
-        std::copy(pl.merges.begin(), pl.merges.end(), h.begin() + 2 * L);
-        cudaMemcpyAsync(b_plan.p, h.data(), smem, cudaMemcpyHostToDevice, st);
+        std::vector<int32_t> h;
+        h.reserve(plan_words);
+        h.insert(h.end(), pl.leaf_off.begin(), pl.leaf_off.end());
+        h.insert(h.end(), pl.leaf_len.begin(), pl.leaf_len.end());
+        int32_t acc = 0;
+        for (int k = 0; k <= n_heights; k++) {
+            h.push_back(acc);
+            if (k < n_heights) acc += (int32_t)pl.by_height[k].size() / 2;
+        }
+        for (auto& v : pl.by_height) h.insert(h.end(), v.begin(), v.end());
+        cudaMemcpyAsync(b_plan.p, h.data(), sizeof(int32_t) * h.size(), cudaMemcpyHostToDevice, st);
         if ((rc = check_cuda(cudaStreamSynchronize(st), "plan upload"))) return rc;  // h dies here
     }
     cudaFuncSetAttribute(row_stats_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 16));
@@ -643,11 +661,11 @@ extern "C" int cs_rep_stats_impl(const double* d_resp, int32_t n_groups, int64_t
         if (max_brackets <= 3)
             row_stats_kernel<3><<<blocks, LB_WARPS * 32, std::max<size_t>(smem, 16), st>>>(
                 d_resp, n_rows, rows_per_group, ldr, m, b_plan.as<int32_t>(), L, d_summ, d_row_sums, do_bracket,
-                nl, lo, hi, off, cap, fill, below, cand);
+                nl, lo, hi, off, cap, fill, below, cand, n_heights);
         else
             row_stats_kernel<MAX_LISTS><<<blocks, LB_WARPS * 32, std::max<size_t>(smem, 16), st>>>(
                 d_resp, n_rows, rows_per_group, ldr, m, b_plan.as<int32_t>(), L, d_summ, d_row_sums, do_bracket,
-                nl, lo, hi, off, cap, fill, below, cand);
+                nl, lo, hi, off, cap, fill, below, cand, n_heights);
         return check_launch("row_stats_kernel");
     };
     auto combine = [&]() { return CS_OK; };  // the tree is combined on chip
