@@ -136,7 +136,14 @@ def ncu_traffic(kernel: str, jobs: int, reps: int, points: int):
         return None
     with open(path) as fh:
         k = json.load(fh)["kernels"].get(kernel)
-    return None if k is None else k["dram_read_bytes"] + k["dram_write_bytes"]
+    return None if k is None else int(k["dram_read_bytes"] + k["dram_write_bytes"])
+
+
+def sim_kernel_name(K: int, C: int, jobs: int) -> str:
+    """The simulator kernel cs_jffc_sim dispatches to (jffc_sim.cu:sim_path)."""
+    if K == 1 and C <= 16:
+        return "jffc_sim_k1_kernel"
+    return "jffc_sim_reg_kernel" if K <= 8 and C <= 16 else "jffc_sim_warp_kernel"
 
 
 def cpu_baseline(rates, caps, lams, args, reps=None):
@@ -283,6 +290,8 @@ def main():
                  + args.points * R * (128 + 8 * eng.ldb))
     peak, peak_kind = measured_peaks()
     achieved = alg_bytes / (sim_ms / 1e3) / 1e9
+    kname = sim_kernel_name(len(rates), int(sum(caps)), args.jobs)
+    stats_bytes = 8 * args.points * R * eng.m  # one read of every stored response
 
     # end to end through the public API (host buffers in/out), rank-local work
     cfgs = [P.SimConfig(rates=rates, capacities=caps, workload=P.PoissonWorkload(l),
@@ -331,10 +340,18 @@ def main():
             "stages_ms": {"streams": streams_ms, "jffc_sim": sim_ms, "stats": stats_ms},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak,
-                         "traffic": ncu_traffic("jffc_sim_reg_kernel", args.jobs, R, args.points),
-                         "algorithmic_bytes": alg_bytes, "kernel": "jffc_sim_reg_kernel",
+                         "traffic": ncu_traffic(kname, args.jobs, R, args.points),
+                         "algorithmic_bytes": alg_bytes, "kernel": kname,
                          "peak_source": peak_kind,
-                         "note": "latency-bound serial event loops; see DESIGN.md roofline"},
+                         "note": "the dominant kernel is issue/latency-bound (serial per-replication "
+                                 "recursions, one warp per scheduler; ncu issue-slot utilisation in "
+                                 "profiles/r1_ncu_full_summary.txt), not HBM-bound; see DESIGN.md §4",
+                         "stats_pass": {"kernel": "row_stats_kernel", "bound": "hbm",
+                                        "algorithmic_bytes": stats_bytes,
+                                        "achieved": stats_bytes / (stats_ms / 1e3) / 1e9,
+                                        "frac": stats_bytes / (stats_ms / 1e3) / 1e9 / peak,
+                                        "note": "whole statistics stage time (sample select + full "
+                                                "row pass + rounds) against the one full read"}},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "jobs/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
