@@ -16,6 +16,7 @@ GPU and bit-exact.
 from __future__ import annotations
 
 import ctypes as C
+import functools
 import math
 from dataclasses import dataclass
 from typing import Sequence
@@ -174,10 +175,10 @@ def _lerp(a: float, b: float, t: float) -> float:
 
 
 def _naive_sum(values) -> float:
-    acc = 0.0
-    for x in values:
-        acc = acc + float(x)
-    return acc
+    """Left-to-right float sum from 0.0 (builtin sum() over np.float64s);
+    np.add.accumulate is sequential, so its last element is that sum."""
+    x = np.asarray(values, dtype=np.float64)
+    return float(np.add.accumulate(x)[-1]) if x.size else 0.0
 
 
 def _nanmean(values) -> float:
@@ -186,13 +187,19 @@ def _nanmean(values) -> float:
     return float(finite.mean()) if finite.size else math.nan
 
 
-def _ci_half_width(values) -> float:
+@functools.lru_cache(maxsize=64)
+def _t975(df: int) -> float:
     from scipy import stats as _st
 
+    return _st.t.ppf(0.975, df)
+
+
+def _ci_half_width(values) -> float:
+    """sim.py:383-388 (the t quantile per degrees of freedom is cached)."""
     x = np.asarray(values, dtype=float)
     if x.size < 2 or np.any(np.isnan(x)):
         return math.nan
-    return float(_st.t.ppf(0.975, x.size - 1) * x.std(ddof=1) / math.sqrt(x.size))
+    return float(_t975(x.size - 1) * x.std(ddof=1) / math.sqrt(x.size))
 
 
 def _require_supported(cfg: SimConfig) -> None:
@@ -210,23 +217,24 @@ def _stats_from(cfg: SimConfig, summ: np.ndarray, busy: np.ndarray, order_stats:
     R = cfg.replications
     if np.any(summ["counted"] < 0):  # jffc_sim_k1_kernel merge-feed overflow (never seen)
         raise AssertionError("simulation merge feed overflowed (exact finish-time ties)")
-    counted = int(sum(int(c) for c in summ["counted"]))
-    rep_means = tuple(float(x) for x in summ["resp_mean"])
-    rep_occ = tuple(float(x) for x in summ["mean_occupancy"])
+    counted = int(summ["counted"].sum())
+    rep_means = tuple(summ["resp_mean"].tolist())
+    rep_occ = tuple(summ["mean_occupancy"].tolist())
     # sim.py:410-411 sums np.float64 values, so builtin sum() is the naive
     # left-to-right sum there (CPython compensates exact floats only)
     total_wait = _naive_sum(summ["wait_sum"])
     total_service = _naive_sum(summ["service_sum"])
     mean_occ = _nanmean(rep_occ)
-    lam_eff = _nanmean([float(x) for x in summ["lambda_effective"]])
+    lam_eff = _nanmean(summ["lambda_effective"])
     # merged.mean(): correctly rounded sum of the per-rep pairwise sums
-    mean_resp = math.fsum(float(x) for x in summ["resp_sum"]) / counted
+    mean_resp = math.fsum(summ["resp_sum"].tolist()) / counted
     caps = cfg.capacities
-    windows = [float(w) for w in summ["window_s"]]
-    util = tuple(
-        _nanmean([float(busy[r, k]) / (caps[k] * windows[r]) if windows[r] > 0 else math.nan
-                  for r in range(R)])
-        for k in range(len(caps)))
+    windows = np.asarray(summ["window_s"], dtype=np.float64)
+    with np.errstate(divide="ignore", invalid="ignore"):  # same IEEE ops, element-wise
+        util = tuple(
+            _nanmean(np.where(windows > 0, np.asarray(busy[:R, k], np.float64) / (caps[k] * windows),
+                              math.nan))
+            for k in range(len(caps)))
     little = (abs(mean_occ - lam_eff * mean_resp) / mean_occ
               if mean_occ and not math.isnan(mean_occ) else math.nan)
     qv = {}
@@ -250,9 +258,9 @@ def _stats_from(cfg: SimConfig, summ: np.ndarray, busy: np.ndarray, order_stats:
         lambda_effective=lam_eff, little_law_gap=little,
         unstable=unstable, seed=cfg.seed, replications=R,
         rep_mean_response_s=rep_means, rep_mean_occupancy=rep_occ,
-        occ_first_half=_nanmean([float(x) for x in summ["occ_first_half"]]),
-        occ_second_half=_nanmean([float(x) for x in summ["occ_second_half"]]),
-        end_queue_len=int(max(int(x) for x in summ["end_queue_len"])), job_records=records)
+        occ_first_half=_nanmean(summ["occ_first_half"]),
+        occ_second_half=_nanmean(summ["occ_second_half"]),
+        end_queue_len=int(summ["end_queue_len"].max()), job_records=records)
 
 
 @dataclass
