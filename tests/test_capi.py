@@ -78,3 +78,50 @@ def test_struct_layouts_match_header():
     assert C.sizeof(N.SimPoint) == 16
     assert C.sizeof(N.RepSummary) == 16 * 8
     assert C.sizeof(N.ComposePoint) == 8 + 4 * 8 + 16
+
+
+def test_extended_entry_points_are_declared():
+    syms = declared_symbols()
+    for s in ("cs_occupancy_bounds", "cs_birth_death_occupancy", "cs_sim_ext", "cs_ragged_rows"):
+        assert s in syms
+
+
+def test_extended_calls_refuse_without_device(lib):
+    from paper_2604_14993_b200 import _native as N
+
+    if lib.cs_device_count() > 0:
+        pytest.skip("a CUDA device is present")
+    assert lib.cs_occupancy_bounds(None, 1, None, None, 1, None, None, None) == N.CS_ERR_CUDA
+    assert lib.cs_birth_death_occupancy(None, 1, None, 1, None, None, None) == N.CS_ERR_CUDA
+    assert lib.cs_sim_ext(None, None) == N.CS_ERR_CUDA
+    assert lib.cs_ragged_rows(None, 1, 1, None, None, None) == N.CS_ERR_CUDA
+
+
+def test_ctypes_layouts_match_the_c_compiler(tmp_path):
+    """sizeof/offsetof of the boundary structs as gcc lays them out from
+    include/chainserve_b200.h == the ctypes mirrors in _native / sim_ext."""
+    import shutil
+    import subprocess
+
+    from paper_2604_14993_b200 import _native as N
+    from paper_2604_14993_b200.sim_ext import ExtArgs
+
+    gcc = shutil.which("gcc") or shutil.which("cc")
+    if gcc is None:
+        pytest.skip("no C compiler")
+    fields = [f for f, _ in ExtArgs._fields_]
+    src = tmp_path / "layout.c"
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "chainserve_b200.h"', "int main(void) {",
+             'printf("%zu %zu %zu %zu %zu\\n", sizeof(cs_sim_ext_args), sizeof(cs_bounds_out), '
+             'sizeof(cs_bound_point), sizeof(cs_bd_point), sizeof(cs_rep_summary));']
+    for f in fields:
+        lines.append(f'printf("%zu\\n", offsetof(cs_sim_ext_args, {f}));')
+    lines.append("return 0; }")
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run([gcc, "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()
+    sizes = [int(x) for x in out[:5]]
+    assert sizes == [C.sizeof(ExtArgs), N.BOUNDS_DTYPE.itemsize, C.sizeof(N.BoundPoint),
+                     C.sizeof(N.BdPoint), C.sizeof(N.RepSummary)]
+    assert [int(x) for x in out[5:]] == [getattr(ExtArgs, f).offset for f in fields]
