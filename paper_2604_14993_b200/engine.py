@@ -75,10 +75,10 @@ class SweepEngine:
                                         reps, N.ptr(keys, C.c_uint64)), "cs_philox_keys")
         self.h_keys = keys
         self.d_keys = torch.from_numpy(keys.view(np.int64)).to(dev)
-        self.d_S = torch.empty(reps * self.lds + 512, dtype=f64, device=dev)  # + CS_STREAM_PAD
-        self.d_resp = torch.empty(self.P * reps * self.ldr, dtype=f64, device=dev)
-        self.d_busy = torch.empty(self.P * reps * self.ldb, dtype=f64, device=dev)
-        self.d_summ = torch.empty(self.P * reps * C.sizeof(N.RepSummary), dtype=torch.uint8, device=dev)
+        # buffer sets: one for step(), a second one for the pipelined sweep
+        self.sets = [self._alloc_set()]
+        self.d_S, self.d_resp = self.sets[0]["S"], self.sets[0]["resp"]
+        self.d_busy, self.d_summ = self.sets[0]["busy"], self.sets[0]["summ"]
         wsb = self.lib.cs_jffc_sim_workspace_bytes(self.P, reps, self.max_chains, self.max_cap, n_jobs)
         self.d_ws = torch.empty(max(wsb, 16), dtype=torch.uint8, device=dev)
         self.ws_bytes = wsb
@@ -91,26 +91,82 @@ class SweepEngine:
         self.h_summ = np.zeros(self.P * reps, N.SUMMARY_DTYPE)
         self.stream = torch.cuda.current_stream()
 
-    # -- stages -----------------------------------------------------------
-    def streams(self):
-        st = self.lib.cs_exp_streams(self.d_keys.data_ptr(), self.R, self.lds, self.d_S.data_ptr(),
-                                     self.lds, self.log1p_variant, self.stream.cuda_stream)
-        N.check(st, "cs_exp_streams")
+    def _alloc_set(self):
+        torch, dev, f64 = self.torch, "cuda", self.torch.float64
+        return {"S": torch.empty(self.R * self.lds + 512, dtype=f64, device=dev),  # + CS_STREAM_PAD
+                "resp": torch.empty(self.P * self.R * self.ldr, dtype=f64, device=dev),
+                "busy": torch.empty(self.P * self.R * self.ldb, dtype=f64, device=dev),
+                "summ": torch.empty(self.P * self.R * C.sizeof(N.RepSummary), dtype=torch.uint8,
+                                    device=dev)}
 
-    def simulate(self):
-        st = self.lib.cs_jffc_sim(
+    # -- stages (buffer set b, CUDA stream st) ------------------------------
+    def streams(self, b: int = 0, st=None):
+        st = st or self.stream
+        S = self.sets[b]["S"]
+        rc = self.lib.cs_exp_streams(self.d_keys.data_ptr(), self.R, self.lds, S.data_ptr(), self.lds,
+                                     self.log1p_variant, st.cuda_stream)
+        N.check(rc, "cs_exp_streams")
+
+    def simulate(self, b: int = 0, st=None):
+        st = st or self.stream
+        B = self.sets[b]
+        rc = self.lib.cs_jffc_sim(
             self.d_pts.data_ptr(), self.P, self.d_rates.data_ptr(), self.d_caps.data_ptr(),
-            self.max_chains, self.max_cap, self.d_S.data_ptr(), self.lds, 0, self.R, self.R, self.n,
-            self.warm, self.d_resp.data_ptr(), self.ldr, self.d_busy.data_ptr(), self.ldb,
-            self.d_summ.data_ptr(), None, self.d_ws.data_ptr(), self.ws_bytes, self.stream.cuda_stream)
-        N.check(st, "cs_jffc_sim")
+            self.max_chains, self.max_cap, B["S"].data_ptr(), self.lds, 0, self.R, self.R, self.n,
+            self.warm, B["resp"].data_ptr(), self.ldr, B["busy"].data_ptr(), self.ldb,
+            B["summ"].data_ptr(), None, self.d_ws.data_ptr(), self.ws_bytes, st.cuda_stream)
+        N.check(rc, "cs_jffc_sim")
 
-    def statistics(self):
+    def statistics(self, b: int = 0, st=None):
+        st = st or self.stream
+        B = self.sets[b]
         fn = self.lib.cs_rep_stats_dist if self.distributed else self.lib.cs_rep_stats
-        st = fn(self.d_resp.data_ptr(), self.P, self.R, self.m, self.ldr, self.d_summ.data_ptr(),
+        rc = fn(B["resp"].data_ptr(), self.P, self.R, self.m, self.ldr, B["summ"].data_ptr(),
                 N.ptr(self.ranks, C.c_int64), len(self.rank_list), N.ptr(self.out_vals, C.c_double),
-                None, self.stream.cuda_stream)
-        N.check(st, "cs_rep_stats")
+                None, st.cuda_stream)
+        N.check(rc, "cs_rep_stats")
+
+    def run_pipelined(self, steps: int, after_stats=None) -> int:
+        """`steps` complete sweeps, software-pipelined over two buffer sets and
+        three CUDA streams: the streams of sweep k+1 and the statistics of
+        sweep k-1 run while sweep k simulates (the simulator leaves most issue
+        slots idle: one latency-bound warp per scheduler).  Every sweep is
+        computed in full; the caller's stream waits for all of them.
+        ``after_stats(b, stream)`` runs after each sweep's statistics (e.g. the
+        cross-GPU gather of its summaries).  Returns the last sweep's set."""
+        torch = self.torch
+        if len(self.sets) < 2:
+            self.sets.append(self._alloc_set())
+            self.pipe = [torch.cuda.Stream() for _ in range(3)]
+        s_gen, s_sim, s_stat = self.pipe
+        cur = torch.cuda.current_stream()
+        for s_ in self.pipe:
+            s_.wait_stream(cur)
+        ev_sim = [torch.cuda.Event(), torch.cuda.Event()]
+        ev_stat = [torch.cuda.Event(), torch.cuda.Event()]
+        ev_gen = [torch.cuda.Event(), torch.cuda.Event()]
+        for k in range(steps + 1):
+            if k < steps:
+                b = k & 1
+                if k >= 2:
+                    s_gen.wait_event(ev_sim[b])  # stream buffer b read by sweep k-2
+                self.streams(b, s_gen)
+                ev_gen[b].record(s_gen)
+                s_sim.wait_event(ev_gen[b])
+                if k >= 2:
+                    s_sim.wait_event(ev_stat[b])  # response buffer b read by sweep k-2
+                self.simulate(b, s_sim)
+                ev_sim[b].record(s_sim)
+            if k >= 1:
+                bb = (k - 1) & 1
+                s_stat.wait_event(ev_sim[bb])
+                self.statistics(bb, s_stat)
+                if after_stats is not None:
+                    after_stats(bb, s_stat)
+                ev_stat[bb].record(s_stat)
+        for s_ in self.pipe:
+            cur.wait_stream(s_)
+        return (steps - 1) & 1
 
     def step(self, timed: bool = False) -> StageTimes | None:
         """One full sweep on the device; optional per-stage CUDA-event times."""
@@ -131,12 +187,12 @@ class SweepEngine:
         ev[3].synchronize()
         return StageTimes(ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2]), ev[2].elapsed_time(ev[3]))
 
-    def summaries(self) -> np.ndarray:
-        self.h_summ[:] = self.d_summ.cpu().numpy().view(N.SUMMARY_DTYPE)
+    def summaries(self, b: int = 0) -> np.ndarray:
+        self.h_summ[:] = self.sets[b]["summ"].cpu().numpy().view(N.SUMMARY_DTYPE)
         return self.h_summ.reshape(self.P, self.R)
 
-    def busy(self) -> np.ndarray:
-        return self.d_busy.cpu().numpy().reshape(self.P, self.R, self.ldb)
+    def busy(self, b: int = 0) -> np.ndarray:
+        return self.sets[b]["busy"].cpu().numpy().reshape(self.P, self.R, self.ldb)
 
     def order_stats(self) -> list[dict]:
         k = len(self.rank_list)

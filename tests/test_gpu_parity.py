@@ -281,3 +281,26 @@ def test_sample_select_and_fused_pairwise_means(eng, oracle):
             assert same_float(v, merged[rank]), (p, rank, v, merged[rank])
         means = np.array([row.mean() for row in resp])
         assert np.array_equal(bits(res.summaries[p]["resp_mean"]), bits(means))
+
+
+def test_sweep_engine_pipelined_equals_unpipelined(eng):
+    """SweepEngine.run_pipelined (two buffer sets, three CUDA streams; the
+    benchmark's timed loop) computes every sweep exactly like step()."""
+    import torch
+
+    from paper_2604_14993_b200.engine import SweepEngine
+
+    service, servers, _ = eng.petals_instance(10, 0.2, 101)
+    system = eng.greedy_cache_allocation(
+        eng.greedy_block_placement(servers, service, 7, 0.2, 0.7).placement)
+    lams = [system.total_rate * x for x in (0.3, 0.9)]
+    e = SweepEngine([system.rates] * 2, [system.capacities] * 2, lams, 20_000, 0.1, 1, 64)
+    e.step()
+    torch.cuda.synchronize()
+    ref_s, ref_b, ref_o = e.summaries(0).copy(), e.busy(0).copy(), e.order_stats()
+    last = e.run_pipelined(3)
+    torch.cuda.synchronize()
+    for b in (0, 1):  # both buffer sets hold a complete, identical sweep
+        assert np.array_equal(e.summaries(b).view(np.uint8), ref_s.view(np.uint8)), b
+        assert np.array_equal(bits(e.busy(b)), bits(ref_b)), b
+    assert e.order_stats() == ref_o and last == 0
