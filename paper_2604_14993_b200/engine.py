@@ -145,18 +145,25 @@ class SweepEngine:
         ev_sim = [torch.cuda.Event(), torch.cuda.Event()]
         ev_stat = [torch.cuda.Event(), torch.cuda.Event()]
         ev_gen = [torch.cuda.Event(), torch.cuda.Event()]
+        def gen(k):  # streams of sweep k into set k & 1 (free once sweep k-2 simulated)
+            b = k & 1
+            if k >= 2:
+                s_gen.wait_event(ev_sim[b])
+            self.streams(b, s_gen)
+            ev_gen[b].record(s_gen)
+
+        if steps > 0:
+            gen(0)
         for k in range(steps + 1):
             if k < steps:
                 b = k & 1
-                if k >= 2:
-                    s_gen.wait_event(ev_sim[b])  # stream buffer b read by sweep k-2
-                self.streams(b, s_gen)
-                ev_gen[b].record(s_gen)
                 s_sim.wait_event(ev_gen[b])
                 if k >= 2:
                     s_sim.wait_event(ev_stat[b])  # response buffer b read by sweep k-2
                 self.simulate(b, s_sim)
                 ev_sim[b].record(s_sim)
+                if k + 1 < steps:  # enqueued before the (host-blocking) statistics below
+                    gen(k + 1)
             if k >= 1:
                 bb = (k - 1) & 1
                 s_stat.wait_event(ev_sim[bb])
