@@ -154,6 +154,24 @@ class SweepEngine:
 
         if steps > 0:
             gen(0)
+        if self.distributed:
+            # sharded: the statistics' NCCL collectives cannot run beside the
+            # simulator (their kernels need an SM configuration the simulator's
+            # SMs do not offer), so statistics follow each simulation in order
+            # and only the streams of the next sweep overlap it
+            for k in range(steps):
+                b = k & 1
+                s_sim.wait_event(ev_gen[b])
+                self.simulate(b, s_sim)
+                ev_sim[b].record(s_sim)
+                if k + 1 < steps:
+                    gen(k + 1)
+                self.statistics(b, s_sim)
+                if after_stats is not None:
+                    after_stats(b, s_sim)
+            for s_ in self.pipe:
+                cur.wait_stream(s_)
+            return (steps - 1) & 1
         for k in range(steps + 1):
             if k < steps:
                 b = k & 1
