@@ -138,15 +138,17 @@ def _chain_set(K, C, seed):
     return rates, tuple(caps)
 
 
-# (K, C) per kernel path: warp kernel SPL x KPL variants, then the generic
-# (workspace heap) kernel beyond 512 slots
-LARGE_CASES = [(3, 20), (12, 40), (40, 100), (70, 200), (20, 400), (2, 600)]
+# (K, C) per kernel path: warp kernel SPL x KPL variants (up to K = 512,
+# C = 1024: the J=1000 full-fleet compositions), then the generic
+# (workspace heap) kernel beyond
+LARGE_CASES = [(3, 20), (12, 40), (40, 100), (70, 200), (20, 400), (2, 600), (300, 700),
+               (2, 1100), (600, 1200)]
 
 
 @pytest.mark.parametrize("K,C", LARGE_CASES)
 def test_large_composition_kernels(eng, oracle, K, C):
     """Compositions beyond the register kernel (K > 8 or C > 16): warp-per-
-    replication kernel, and the generic kernel for C > 512."""
+    replication kernel, and the generic kernel for K > 512 or C > 1024."""
     rates, caps = _chain_set(K, C, K * 1000 + C)
     lam = 0.9 * sum(r * c for r, c in zip(rates, caps))
     n, R = 6000, 5
