@@ -192,13 +192,15 @@ __global__ void __launch_bounds__(LB_WARPS * 32) row_stats_kernel(
     double* __restrict__ row_sums, int do_bracket, const int32_t* __restrict__ grp_nlist,
     const uint64_t* __restrict__ lo, const uint64_t* __restrict__ hi, const int64_t* __restrict__ off,
     const int64_t* __restrict__ cap, unsigned long long* __restrict__ fill,
-    unsigned long long* __restrict__ below, double* __restrict__ cand, int32_t n_heights) {
+    unsigned long long* __restrict__ below, double* __restrict__ cand, int32_t n_heights,
+    double* __restrict__ leaf_scratch) {
     // shared: per-warp leaf values [LB_WARPS][L] doubles, then the plan:
     // leaf offset[L], leaf length[L], height offsets[n_heights + 1] and the
     // internal nodes in height order as (a, b) pairs: v[a] = v[a] + v[b]
     // (a = the node's leftmost leaf, b = its right child's leftmost leaf)
+    // leaf values: shared memory, or (long rows) a global scratch slice per warp
     extern __shared__ double row_sh[];
-    int32_t* plan = reinterpret_cast<int32_t*>(row_sh + (size_t)LB_WARPS * L);
+    int32_t* plan = reinterpret_cast<int32_t*>(leaf_scratch ? row_sh : row_sh + (size_t)LB_WARPS * L);
     const int plan_words = 2 * L + (n_heights + 1) + 2 * (L - 1);
     for (int q = threadIdx.x; q < plan_words; q += blockDim.x) plan[q] = g_plan[q];
     __syncthreads();
@@ -206,7 +208,9 @@ __global__ void __launch_bounds__(LB_WARPS * 32) row_stats_kernel(
     const int32_t* leaf_len = plan + L;
     const int32_t* h_off = plan + 2 * L;
     const int32_t* nodes = h_off + n_heights + 1;
-    double* lv = row_sh + (size_t)(threadIdx.x >> 5) * L;
+    double* lv = leaf_scratch
+                     ? leaf_scratch + ((size_t)blockIdx.x * LB_WARPS + (threadIdx.x >> 5)) * (size_t)L
+                     : row_sh + (size_t)(threadIdx.x >> 5) * L;
     const int lane = threadIdx.x & 31, j = lane & 7, sub = lane >> 3, warp = threadIdx.x >> 5;
     for (int64_t row = (int64_t)blockIdx.x * LB_WARPS + warp; row < n_rows; row += (int64_t)gridDim.x * LB_WARPS) {
         const int64_t g = row / rows_per_group;
@@ -628,7 +632,9 @@ extern "C" int cs_rep_stats_impl(const double* d_resp, int32_t n_groups, int64_t
     const int32_t L = (int32_t)pl.leaf_off.size();
     const int32_t n_heights = (int32_t)pl.by_height.size();
     const size_t plan_words = 2 * (size_t)L + n_heights + 1 + 2 * (size_t)std::max(L - 1, 0);
-    const size_t smem = sizeof(double) * LB_WARPS * (size_t)L + sizeof(int32_t) * plan_words;
+    const size_t plan_bytes = sizeof(int32_t) * plan_words;
+    const bool leaves_in_smem = sizeof(double) * LB_WARPS * (size_t)L + plan_bytes <= 160 * 1024;
+    const size_t smem = (leaves_in_smem ? sizeof(double) * LB_WARPS * (size_t)L : 0) + plan_bytes;
     if (smem > 200 * 1024) {
         set_error("cs_rep_stats: rows of %lld responses exceed the on-chip pairwise plan", (long long)m);
         return CS_UNSUPPORTED;
@@ -654,6 +660,10 @@ extern "C" int cs_rep_stats_impl(const double* d_resp, int32_t n_groups, int64_t
                          (int)std::max<size_t>(smem, 16));
     const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((n_rows + LB_WARPS - 1) / LB_WARPS,
                                                                    (int64_t)sm_count() * 8));
+    DBuf b_leaf;  // long rows: leaf values in global scratch (one slice per resident warp)
+    if (!leaves_in_smem && (rc = b_leaf.alloc(sizeof(double) * (size_t)blocks * LB_WARPS * (size_t)L, st)))
+        return rc;
+    double* leaf_scratch = leaves_in_smem ? nullptr : b_leaf.as<double>();
     int max_brackets = 0;  // set per bracket attempt; selects the kernel instance
     auto leaf_pass = [&](int do_bracket, const int32_t* nl, const uint64_t* lo, const uint64_t* hi,
                          const int64_t* off, const int64_t* cap, unsigned long long* fill,
@@ -661,11 +671,11 @@ extern "C" int cs_rep_stats_impl(const double* d_resp, int32_t n_groups, int64_t
         if (max_brackets <= 3)
             row_stats_kernel<3><<<blocks, LB_WARPS * 32, std::max<size_t>(smem, 16), st>>>(
                 d_resp, n_rows, rows_per_group, ldr, m, b_plan.as<int32_t>(), L, d_summ, d_row_sums, do_bracket,
-                nl, lo, hi, off, cap, fill, below, cand, n_heights);
+                nl, lo, hi, off, cap, fill, below, cand, n_heights, leaf_scratch);
         else
             row_stats_kernel<MAX_LISTS><<<blocks, LB_WARPS * 32, std::max<size_t>(smem, 16), st>>>(
                 d_resp, n_rows, rows_per_group, ldr, m, b_plan.as<int32_t>(), L, d_summ, d_row_sums, do_bracket,
-                nl, lo, hi, off, cap, fill, below, cand, n_heights);
+                nl, lo, hi, off, cap, fill, below, cand, n_heights, leaf_scratch);
         return check_launch("row_stats_kernel");
     };
     auto combine = [&]() { return CS_OK; };  // the tree is combined on chip

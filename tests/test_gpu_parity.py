@@ -306,3 +306,22 @@ def test_sweep_engine_pipelined_equals_unpipelined(eng):
         assert np.array_equal(e.summaries(b).view(np.uint8), ref_s.view(np.uint8)), b
         assert np.array_equal(bits(e.busy(b)), bits(ref_b)), b
     assert e.order_stats() == ref_o and last == 0
+
+
+def test_long_rows_statistics(eng, oracle):
+    """Rows of 225k responses (the split-tree leaf values spill from shared
+    memory to a global scratch, as for config 5's 9e5-response rows): exact
+    pairwise rep means and order statistics vs the oracle."""
+    rates, caps = (0.9,), (3,)
+    lam = 0.8 * 0.9 * 3
+    n, R = 250_000, 3
+    res = eng.simulate_sweep([rates], [caps], [lam], n, 0.1, 5, R, return_responses=True)
+    allr = []
+    for r in range(R):
+        o = oracle.simulate_once(rates, caps, lam, n, 0.1, 5, r)
+        assert np.array_equal(bits(res.responses[0, r]), bits(o["responses"])), r
+        assert same_float(res.summaries[0, r]["resp_mean"], o["responses"].mean()), r
+        allr.append(o["responses"])
+    merged = np.sort(np.concatenate(allr))
+    for rank, v in res.order_stats[0].items():
+        assert same_float(v, merged[rank]), rank
