@@ -7,7 +7,8 @@ scratch/profile_round.sh (same bench command, N=1, config 2):
                      `bench.py --steps 2 --warmup 3`, cold-cache, serialised)
   prof_dram.csv      ncu --metrics dram__bytes_{read,write}.sum for the
                      simulator, stream and row-statistics kernels
-  prof_full.ncu-rep  ncu --set full of the simulator and row-statistics kernels
+  prof_full.ncu-rep, prof_full_stats.ncu-rep
+                     ncu --set full of the simulator and the row-statistics kernel
 
     python profiles/make_summaries.py r1 [gpurun_out]
 """
@@ -25,8 +26,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 
 
 def _rows(path):
-    with open(path) as fh:
-        lines = [ln for ln in fh if not ln.startswith("==")]
+    with open(path) as fh:  # ncu CSV rows only (the profiled program's stdout may be interleaved)
+        lines = [ln for ln in fh if ln.startswith('"')]
     return list(csv.DictReader(lines))
 
 
@@ -89,8 +90,12 @@ METRICS = ("Duration", "DRAM Throughput", "Memory Throughput", "L1/TEX Hit Rate"
 
 
 def full(tag, src):
-    rep = os.path.join(src, "prof_full.ncu-rep")
-    txt = subprocess.run(["ncu", "-i", rep, "--page", "details"], capture_output=True, text=True).stdout
+    txt = ""
+    for name in ("prof_full.ncu-rep", "prof_full_stats.ncu-rep"):
+        rep = os.path.join(src, name)
+        if os.path.exists(rep):
+            txt += subprocess.run(["ncu", "-i", rep, "--page", "details"], capture_output=True,
+                                  text=True).stdout
     out, kernel = [f"# {tag}: ncu --set full --clock-control none of the top kernels "
                    "(python bench.py --steps 1 --warmup 0 --e2e-steps 0 --no-cpu-baseline)"], None
     for line in txt.splitlines():
