@@ -28,7 +28,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 def _rows(path):
     with open(path) as fh:  # ncu CSV rows only (the profiled program's stdout may be interleaved)
         lines = [ln for ln in fh if ln.startswith('"')]
-    return list(csv.DictReader(lines))
+    hdr = lines[:1]  # captures appended one after another repeat the header
+    return list(csv.DictReader(hdr + [ln for ln in lines[1:] if not ln.startswith('"ID"')]))
 
 
 def short(name: str) -> str:
