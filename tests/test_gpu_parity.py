@@ -325,3 +325,25 @@ def test_long_rows_statistics(eng, oracle):
     merged = np.sort(np.concatenate(allr))
     for rank, v in res.order_stats[0].items():
         assert same_float(v, merged[rank]), rank
+
+
+@pytest.mark.parametrize("C", [1, 3, 4, 7, 8, 12, 16])
+def test_single_chain_kernel_stress(eng, oracle, C):
+    """The single-chain recursion + merge kernel (jffc_sim_k1_kernel) across
+    capacities and loads from light to overloaded (long FCFS queues, lagging
+    merges), plus heavy warm-up: every RepResult field, responses, busy time
+    and job records bit-exact vs the oracle."""
+    rate = 0.7 + 0.05 * C
+    lams = [rho * rate * C for rho in (0.2, 0.95, 1.3)]
+    n, R = 20_000, 4
+    for wf in (0.0, 0.5):
+        res = eng.simulate_sweep([(rate,)] * 3, [(C,)] * 3, lams, n, wf, 23, R, return_responses=True,
+                                 collect_jobs=True)
+        for p, lam in enumerate(lams):
+            for r in range(R):
+                o = oracle.simulate_once((rate,), (C,), lam, n, wf, 23, r, collect_jobs=True)
+                assert np.array_equal(bits(res.responses[p, r]), bits(o["responses"])), (p, r)
+                assert np.array_equal(bits(res.jobs[p, r]), bits(o["jobs"])), (p, r)
+                assert same_float(res.busy[p][r, 0], o["busy_time_s"][0]), (p, r)
+                for f in REP_FIELDS:
+                    assert same_float(res.summaries[p, r][f], o[f]), (p, r, f)
