@@ -74,11 +74,10 @@ def lam_grid(rates, caps, points):
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
-
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clocks and clock-event (throttle) reasons sampled through NVML during
+    the timed region (the nvidia-smi fields clocks.sm, clocks.max.sm and
+    clocks_event_reasons.*).  NVML in-process: spawning nvidia-smi from a
+    thread forks the whole CUDA process and stalls the launch thread."""
 
     def __init__(self, gpu_index: int):
         self.idx = gpu_index
@@ -87,13 +86,21 @@ class ClockSampler:
         self._t = threading.Thread(target=self._run, daemon=True)
 
     def _run(self):
+        try:
+            import pynvml as nv
+
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.idx)
+            bits = (nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                    nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap)
+        except Exception:
+            return
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True,
-                                     text=True, timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([x.strip() for x in out.split(",")])
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.rows.append([str(self.idx), str(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)),
+                                  str(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)), "", ""] +
+                                 ["Active" if r & b else "Not Active" for b in bits])
             except Exception:
                 pass
             self._stop.wait(0.2)
