@@ -28,6 +28,7 @@
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
+#include <time.h>
 
 #include <algorithm>
 #include <utility>
@@ -408,6 +409,19 @@ __global__ void __launch_bounds__(1024) round_select_kernel(SelSlot* __restrict_
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
+// CS_TRACE_STATS=1: host timestamps at the statistics' phase boundaries
+static void trace(const char* what, cudaStream_t st) {
+    static const bool on = getenv("CS_TRACE_STATS") != nullptr;
+    if (!on) return;
+    static double t0 = 0;
+    cudaStreamSynchronize(st);
+    timespec ts;
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    const double t = ts.tv_sec * 1e3 + ts.tv_nsec * 1e-6;
+    if (!strcmp(what, "begin")) t0 = t;
+    fprintf(stderr, "[stats] %-14s %8.3f ms\n", what, t - t0);
+}
+
 struct DBuf {
     void* p = nullptr;
     size_t n = 0;
@@ -482,9 +496,21 @@ static int select_rows(const double* d_resp, int64_t n_groups, int64_t rows_per_
     if (dist && ((rc = allreduce_u32(b_h0.p, (size_t)H0_BINS * n_groups, st)) ||
                  (rc = allreduce_u64(b_bad.p, 1, st))))
         return rc;
-    std::vector<uint32_t> h0((size_t)H0_BINS * n_groups);
-    unsigned long long bad = 0;
-    cudaMemcpyAsync(h0.data(), b_h0.p, b_h0.n, cudaMemcpyDeviceToHost, st);
+    // pinned read-back buffer (2 MB for 16 groups), kept across calls
+    static thread_local uint32_t* h0 = nullptr;
+    static thread_local size_t h0_cap = 0;
+    const size_t h0_need = (size_t)H0_BINS * n_groups + 2;
+    if (h0_cap < h0_need) {
+        if (h0) cudaFreeHost(h0);
+        if ((rc = check_cuda(cudaMallocHost(&h0, sizeof(uint32_t) * h0_need), "cudaMallocHost"))) {
+            h0 = nullptr;
+            h0_cap = 0;
+            return rc;
+        }
+        h0_cap = h0_need;
+    }
+    unsigned long long& bad = *reinterpret_cast<unsigned long long*>(h0 + (size_t)H0_BINS * n_groups);
+    cudaMemcpyAsync(h0, b_h0.p, b_h0.n, cudaMemcpyDeviceToHost, st);
     cudaMemcpyAsync(&bad, b_bad.p, sizeof(bad), cudaMemcpyDeviceToHost, st);
     if ((rc = check_cuda(cudaStreamSynchronize(st), "select hist sync"))) return rc;
     if (bad) {
@@ -496,16 +522,32 @@ static int select_rows(const double* d_resp, int64_t n_groups, int64_t rows_per_
     std::vector<int64_t> off((size_t)n_groups * SEL_LISTS, 0), cap((size_t)n_groups * SEL_LISTS, 0);
     std::vector<SelSlot> slots((size_t)n_groups * n_ranks);
     int64_t total = 0;
+    std::vector<int> order(n_ranks);
+    std::vector<uint32_t> bin_of(n_ranks);
+    std::vector<int64_t> below_of(n_ranks);
     for (int64_t g = 0; g < n_groups; g++) {
-        const uint32_t* hg = h0.data() + (size_t)g * H0_BINS;
-        for (int q = 0; q < n_ranks; q++) {
-            const int64_t rank = ranks[g * n_ranks + q];
+        const uint32_t* hg = h0 + (size_t)g * H0_BINS;
+        // one walk over the bins for all of the group's ranks, in rank order
+        for (int q = 0; q < n_ranks; q++) order[q] = q;
+        std::sort(order.begin(), order.end(),
+                  [&](int x, int y) { return ranks[g * n_ranks + x] < ranks[g * n_ranks + y]; });
+        {
             int64_t c = 0;
             uint32_t b = 0;
-            for (; b < (uint32_t)H0_BINS; b++) {
-                if (c + (int64_t)hg[b] > rank) break;
-                c += hg[b];
+            for (int i = 0; i < n_ranks; i++) {
+                const int64_t rank = ranks[g * n_ranks + order[i]];
+                for (; b < (uint32_t)H0_BINS; b++) {
+                    if (c + (int64_t)hg[b] > rank) break;
+                    c += hg[b];
+                }
+                bin_of[order[i]] = b;
+                below_of[order[i]] = c;
             }
+        }
+        for (int q = 0; q < n_ranks; q++) {
+            const int64_t rank = ranks[g * n_ranks + q];
+            const int64_t c = below_of[q];
+            const uint32_t b = bin_of[q];
             int list = -1;
             for (int l = 0; l < nlist[g]; l++)
                 if (bucket[g * SEL_LISTS + l] == b) list = l;
@@ -719,8 +761,10 @@ extern "C" int cs_rep_stats_impl(const double* d_resp, int32_t n_groups, int64_t
                 r_both[(g * 2 * n_ranks) + n_ranks + q] = r_hi[g * n_ranks + q];
             }
         std::vector<double> v_both, v_lo(T), v_hi(T);
+        trace("begin", st);
         if ((rc = select_rows(d_resp, n_groups, rows_per_group, sample, ldr, r_both, 2 * n_ranks, v_both, dist, st)))
             return rc;
+        trace("sample select", st);
         for (int64_t g = 0; g < n_groups; g++)
             for (int q = 0; q < n_ranks; q++) {
                 v_lo[g * n_ranks + q] = v_both[g * 2 * n_ranks + q];
@@ -781,6 +825,7 @@ extern "C" int cs_rep_stats_impl(const double* d_resp, int32_t n_groups, int64_t
         cudaMemsetAsync(b_fill.p, 0, b_fill.n, st);
         cudaMemsetAsync(b_below.p, 0, b_below.n, st);
         max_brackets = *std::max_element(nlist.begin(), nlist.end());
+        trace("bracket setup", st);
         if ((rc = leaf_pass(1, b_nl.as<int32_t>(), b_lo.as<uint64_t>(), b_hi.as<uint64_t>(), b_off.as<int64_t>(),
                             b_cap.as<int64_t>(), b_fill.as<unsigned long long>(), b_below.as<unsigned long long>(),
                             b_cand.as<double>())))
@@ -805,6 +850,7 @@ extern "C" int cs_rep_stats_impl(const double* d_resp, int32_t n_groups, int64_t
         cudaMemcpyAsync(fill_all.data(), b_fill.p, b_fill.n, cudaMemcpyDeviceToHost, st);
         cudaMemcpyAsync(below.data(), b_below.p, b_below.n, cudaMemcpyDeviceToHost, st);
         if ((rc = check_cuda(cudaStreamSynchronize(st), "bracket sync 2"))) return rc;
+        trace("row pass+counts", st);
         // ---- 3. verify the brackets, exact rounds over the candidates ----
         const int first_shift = (top_bit / RD_BITS) * RD_BITS;  // digits cover bits <= top_bit
         const uint64_t keep = first_shift + RD_BITS >= 64 ? 0ull : ~((1ull << (first_shift + RD_BITS)) - 1);
@@ -830,6 +876,7 @@ extern "C" int cs_rep_stats_impl(const double* d_resp, int32_t n_groups, int64_t
         }
         if (!ok) continue;  // the sample missed a target (or overflowed): widen, retry
         if ((rc = run_rounds(slots, b_cand.as<double>(), first_shift, dist, st))) return rc;
+        trace("cand rounds", st);
         for (size_t i = 0; i < T; i++) memcpy(&out_values[i], &slots[i].prefix, 8);
         return CS_OK;
     }
