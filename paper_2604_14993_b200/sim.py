@@ -224,7 +224,8 @@ def _stats_from(cfg: SimConfig, summ: np.ndarray, busy: np.ndarray, order_stats:
     # left-to-right sum there (CPython compensates exact floats only)
     total_wait = _naive_sum(summ["wait_sum"])
     total_service = _naive_sum(summ["service_sum"])
-    mean_occ = _nanmean(rep_occ)
+    occ_a = np.asarray(summ["mean_occupancy"], dtype=np.float64)
+    mean_occ = _nanmean(occ_a)
     lam_eff = _nanmean(summ["lambda_effective"])
     # merged.mean(): correctly rounded sum of the per-rep pairwise sums
     mean_resp = math.fsum(summ["resp_sum"].tolist()) / counted
@@ -253,8 +254,9 @@ def _stats_from(cfg: SimConfig, summ: np.ndarray, busy: np.ndarray, order_stats:
         policy=cfg.policy, jobs_counted=counted, mean_response_s=mean_resp,
         median_response_s=qv[0.5], p95_response_s=qv[0.95], p99_response_s=qv[0.99],
         mean_waiting_s=total_wait / counted, mean_service_s=total_service / counted,
-        mean_occupancy=mean_occ, response_ci_half_width_s=_ci_half_width(rep_means),
-        occupancy_ci_half_width=_ci_half_width(rep_occ), per_chain_utilization=util,
+        mean_occupancy=mean_occ,
+        response_ci_half_width_s=_ci_half_width(np.asarray(summ["resp_mean"], dtype=np.float64)),
+        occupancy_ci_half_width=_ci_half_width(occ_a), per_chain_utilization=util,
         lambda_effective=lam_eff, little_law_gap=little,
         unstable=unstable, seed=cfg.seed, replications=R,
         rep_mean_response_s=rep_means, rep_mean_occupancy=rep_occ,
