@@ -83,14 +83,21 @@ __global__ void __launch_bounds__(1024) hist0_rows_kernel(const double* __restri
         for (int b = threadIdx.x; b < H0_BINS; b += blockDim.x) sh[b] = 0;
         __syncthreads();
         const int64_t ga = max(r0, g * rows_per_group), gb = min(r1, (g + 1) * rows_per_group);
-        for (int64_t row = ga; row < gb; row++) {
-            const double* __restrict__ a = resp + row * ldr;
+        constexpr int R = 4;  // rows in flight per thread (memory-level parallelism)
+        for (int64_t row = ga; row < gb; row += R) {
             for (int64_t s = threadIdx.x; s < rv.len; s += blockDim.x) {
-                const uint64_t u = dbits(a[rv.phys(s)]);
-                if (u >> 63)
-                    atomicAdd(n_bad, 1ull);
-                else
-                    atomicAdd(&sh[u >> 48], 1u);
+                const int64_t ps = rv.phys(s);
+                uint64_t u[R];
+#pragma unroll
+                for (int r = 0; r < R; r++) u[r] = row + r < gb ? dbits(__ldg(resp + (row + r) * ldr + ps)) : 0ull;
+#pragma unroll
+                for (int r = 0; r < R; r++) {
+                    if (row + r >= gb) continue;
+                    if (u[r] >> 63)
+                        atomicAdd(n_bad, 1ull);
+                    else
+                        atomicAdd(&sh[u[r] >> 48], 1u);
+                }
             }
         }
         __syncthreads();
@@ -119,34 +126,126 @@ __device__ __forceinline__ void append(int list, double v, unsigned long long* _
     }
 }
 
-// Compaction of the values whose digit 0 is one of the group's selected buckets.
-__global__ void compact_bucket_kernel(const double* __restrict__ resp, int64_t n_rows, RowView rv,
-                                      int64_t ldr, int64_t rows_per_group,
-                                      const int32_t* __restrict__ grp_nlist,
-                                      const uint32_t* __restrict__ grp_bucket,
-                                      const int64_t* __restrict__ off, const int64_t* __restrict__ cap,
-                                      unsigned long long* __restrict__ fill, double* __restrict__ cand) {
-    for (int64_t row = blockIdx.x; row < n_rows; row += gridDim.x) {
+// Candidate appends without a returning atomic on the critical path: lane q
+// owns list q's reservation of CAND_CHUNK slots (base, used) and the next
+// reservation, requested a whole chunk ahead (next), so the atomic's latency
+// is hidden behind the chunk's appends.  Reserved slots that stay unused hold
+// the sentinel (all ones: above every response's bit pattern), which never
+// changes a rank counted from below.
+constexpr int CAND_CHUNK = 32;  // == warp size: sealing is one store per lane
+struct CandChunks {
+    unsigned long long base, next;
+    int used;
+    uint32_t in;  // values appended (owner lane)
+};
+
+__device__ __forceinline__ void cand_open(CandChunks& c, int lane, int nl, unsigned long long* __restrict__ fill_g) {
+    c.base = c.next = 0;
+    c.used = 0;
+    c.in = 0;
+    if (lane < nl) {
+        c.base = atomicAdd(&fill_g[lane], (unsigned long long)CAND_CHUNK);
+        c.next = atomicAdd(&fill_g[lane], (unsigned long long)CAND_CHUNK);
+    }
+}
+
+// Append w to local list ql (every lane calls it; ql < 0: nothing) -- the
+// part for list q; the caller loops q over the lists.
+__device__ __forceinline__ void cand_push(CandChunks& c, int lane, int q, int ql, double w,
+                                          unsigned long long* __restrict__ fill_g,
+                                          const int64_t* __restrict__ cap_g, const int64_t* __restrict__ off_g,
+                                          double* __restrict__ cand) {
+    const unsigned msk = __ballot_sync(0xffffffffu, ql == q);
+    if (msk == 0) return;
+    const int cnt = __popc(msk);
+    const int u = __shfl_sync(0xffffffffu, c.used, q);
+    const unsigned long long b = __shfl_sync(0xffffffffu, c.base, q);
+    const int pos = u + __popc(msk & ((1u << lane) - 1u));
+    unsigned long long slot = b + (unsigned long long)pos;
+    if (u + cnt > CAND_CHUNK) {  // this append crosses into the next reservation
+        const unsigned long long nb = __shfl_sync(0xffffffffu, c.next, q);
+        if (pos >= CAND_CHUNK) slot = nb + (unsigned long long)(pos - CAND_CHUNK);
+        if (lane == q) {
+            c.base = nb;
+            c.used = u + cnt - CAND_CHUNK;
+            c.next = atomicAdd(&fill_g[q], (unsigned long long)CAND_CHUNK);
+        }
+    } else if (lane == q) {
+        c.used = u + cnt;
+    }
+    if (lane == q) c.in += (uint32_t)cnt;
+    if (ql == q && slot < (unsigned long long)cap_g[q]) cand[off_g[q] + slot] = w;  // overflow: host check
+}
+
+// Seal the reservations: the current one's tail and the untouched next one.
+__device__ __forceinline__ void cand_seal(const CandChunks& c, int lane, int nl, const int64_t* __restrict__ cap_g,
+                                          const int64_t* __restrict__ off_g, double* __restrict__ cand) {
+    const double sent = __longlong_as_double(-1ll);
+    for (int q = 0; q < nl; q++) {
+        const int u = __shfl_sync(0xffffffffu, c.used, q);
+        const unsigned long long b = __shfl_sync(0xffffffffu, c.base, q);
+        const unsigned long long nb = __shfl_sync(0xffffffffu, c.next, q);
+        const unsigned long long cq = (unsigned long long)cap_g[q];
+        if (u + lane < CAND_CHUNK && b + u + lane < cq) cand[off_g[q] + b + u + lane] = sent;
+        if (nb + lane < cq) cand[off_g[q] + nb + lane] = sent;
+    }
+}
+
+// Compaction of the values whose digit 0 is one of the group's selected
+// buckets: a warp per row, chunked appends (the lists are pre-set to the
+// sentinel, so no sealing).
+__global__ void __launch_bounds__(256) compact_bucket_kernel(
+    const double* __restrict__ resp, int64_t n_rows, RowView rv, int64_t ldr, int64_t rows_per_group,
+    const int32_t* __restrict__ grp_nlist, const uint32_t* __restrict__ grp_bucket,
+    const int64_t* __restrict__ off, const int64_t* __restrict__ cap, unsigned long long* __restrict__ fill,
+    double* __restrict__ cand) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); row < n_rows; row += warps) {
         const int64_t g = row / rows_per_group;
         const int nl = grp_nlist[g];
+        const int64_t gl0 = g * SEL_LISTS;
         uint32_t bk[SEL_LISTS];
 #pragma unroll
-        for (int q = 0; q < SEL_LISTS; q++) bk[q] = q < nl ? grp_bucket[g * SEL_LISTS + q] : 0xffffffffu;
+        for (int q = 0; q < SEL_LISTS; q++) bk[q] = q < nl ? grp_bucket[gl0 + q] : 0xffffffffu;
+        CandChunks cc;
+        cand_open(cc, lane, nl, fill + gl0);
         const double* __restrict__ a = resp + row * ldr;
-        for (int64_t base = 0; base < rv.len; base += blockDim.x) {
-            const int64_t s = base + threadIdx.x;
-            int list = -1;
-            double v = 0.0;
-            if (s < rv.len) {
-                v = a[rv.phys(s)];
-                const uint32_t d0 = (uint32_t)(dbits(v) >> 48);
+        constexpr int U = 8;  // loads in flight per lane
+        for (int64_t base = 0; base < rv.len; base += 32 * U) {
+            double v[U];
 #pragma unroll
-                for (int q = 0; q < SEL_LISTS; q++)
-                    if (bk[q] == d0) list = (int)(g * SEL_LISTS + q);
+            for (int k = 0; k < U; k++) {
+                const int64_t s = base + 32 * k + lane;
+                v[k] = s < rv.len ? __ldg(a + rv.phys(s)) : 0.0;
             }
-            append(list, v, fill, off, cap, cand);
+#pragma unroll
+            for (int k = 0; k < U; k++) {
+                int ql = -1;
+                if (base + 32 * k + lane < rv.len) {
+                    const uint32_t d0 = (uint32_t)(dbits(v[k]) >> 48);
+#pragma unroll
+                    for (int q = 0; q < SEL_LISTS; q++)
+                        if (bk[q] == d0) ql = q;
+                }
+                if (__any_sync(0xffffffffu, ql >= 0))
+                    for (int q = 0; q < nl; q++)
+                        cand_push(cc, lane, q, ql, v[k], fill + gl0, cap + gl0, off + gl0, cand);
+            }
         }
     }
+}
+
+// v[t] for a runtime t without local memory: a 4-level select tree
+__device__ __forceinline__ double pick16(const double (&v)[16], int t) {
+    double l1[8], l2[4], l3[2];
+#pragma unroll
+    for (int i = 0; i < 8; i++) l1[i] = (t & 1) ? v[2 * i + 1] : v[2 * i];
+#pragma unroll
+    for (int i = 0; i < 4; i++) l2[i] = (t & 2) ? l1[2 * i + 1] : l1[2 * i];
+#pragma unroll
+    for (int i = 0; i < 2; i++) l3[i] = (t & 4) ? l2[2 * i + 1] : l2[2 * i];
+    return (t & 8) ? l3[1] : l3[0];
 }
 
 // Bracket state of one row (registers only: fixed sizes, static indices).
@@ -187,14 +286,14 @@ __device__ __forceinline__ int classify_one(Brackets<NB>& br, uint64_t u, bool h
 constexpr int LB_WARPS = 8;
 
 template <int NB>
-__global__ void __launch_bounds__(LB_WARPS * 32) row_stats_kernel(
+__global__ void __launch_bounds__(LB_WARPS * 32, 2) row_stats_kernel(
     const double* __restrict__ resp, int64_t n_rows, int64_t rows_per_group, int64_t ldr, int64_t m,
     const int32_t* __restrict__ g_plan, int32_t L, cs_rep_summary* __restrict__ summ,
     double* __restrict__ row_sums, int do_bracket, const int32_t* __restrict__ grp_nlist,
     const uint64_t* __restrict__ lo, const uint64_t* __restrict__ hi, const int64_t* __restrict__ off,
     const int64_t* __restrict__ cap, unsigned long long* __restrict__ fill,
-    unsigned long long* __restrict__ below, double* __restrict__ cand, int32_t n_heights,
-    double* __restrict__ leaf_scratch) {
+    unsigned long long* __restrict__ below, unsigned long long* __restrict__ inside,
+    double* __restrict__ cand, int32_t n_heights, double* __restrict__ leaf_scratch) {
     // shared: per-warp leaf values [LB_WARPS][L] doubles, then the plan:
     // leaf offset[L], leaf length[L], height offsets[n_heights + 1] and the
     // internal nodes in height order as (a, b) pairs: v[a] = v[a] + v[b]
@@ -227,73 +326,70 @@ __global__ void __launch_bounds__(LB_WARPS * 32) row_stats_kernel(
             br.cnt[q] = 0;
         }
         const double* __restrict__ rowp = resp + row * ldr;
-        // software pipeline: the next leaf group's loads are in flight while
-        // this group's values are classified and summed
-        double nv[16];
-        {
-            const int leaf = sub;
+        const int64_t gl0 = g * MAX_LISTS;
+        CandChunks cc{0ull, 0ull, 0, 0u};
+        if (do_bracket) cand_open(cc, lane, nl, fill + gl0);
+        auto push = [&](int ql, double w) {  // every lane; ql = local list or -1
+#pragma unroll
+            for (int q = 0; q < NB; q++) cand_push(cc, lane, q, ql, w, fill + gl0, cap + gl0, off + gl0, cand);
+        };
+        // Software pipeline: the next leaf group's loads are in flight while
+        // this group is summed and classified.
+        // Slots past a leaf's 8-aligned end hold +0.0, which leaves the lane
+        // sums unchanged (all values are >= +0) and is counted "below" by the
+        // fast path exactly when 0 < lo_hw; that is undone per lane at the end.
+        uint32_t npad = 0;
+        auto load_group = [&](int leaf0, double (&buf)[16]) {
+            const int leaf = leaf0 + sub;
             const int len = leaf < L ? leaf_len[leaf] : 0;
             const double* __restrict__ a = rowp + (leaf < L ? leaf_off[leaf] : 0);
             const int main_end = len >= 8 ? len - len % 8 : 0;
 #pragma unroll
-            for (int t = 0; t < 16; t++) nv[t] = (j + 8 * t < main_end) ? __ldg(a + j + 8 * t) : 0.0;
-        }
-        for (int l0 = 0; l0 < L; l0 += 4) {
+            for (int t = 0; t < 16; t++) buf[t] = (j + 8 * t < main_end) ? __ldg(a + j + 8 * t) : 0.0;
+        };
+        auto process_group = [&](int l0, const double (&v)[16]) {
             const int leaf = l0 + sub;
             const bool valid = leaf < L;
             const int len = valid ? leaf_len[leaf] : 0;
             const double* __restrict__ a = rowp + (valid ? leaf_off[leaf] : 0);
             const int main_end = len >= 8 ? len - len % 8 : 0;
-            double v[16];
-#pragma unroll
-            for (int t = 0; t < 16; t++) v[t] = nv[t];
-            {
-                const int nleaf = leaf + 4;
-                const int nlen = nleaf < L ? leaf_len[nleaf] : 0;
-                const double* __restrict__ na = rowp + (nleaf < L ? leaf_off[nleaf] : 0);
-                const int nmain = nlen >= 8 ? nlen - nlen % 8 : 0;
-#pragma unroll
-                for (int t = 0; t < 16; t++) nv[t] = (j + 8 * t < nmain) ? __ldg(na + j + 8 * t) : 0.0;
-            }
+            const int nvalid = main_end > j ? (main_end - j + 7) >> 3 : 0;  // slots t < nvalid hold data
             double acc = v[0];
 #pragma unroll
-            for (int t = 1; t < 16; t++)
-                if (j + 8 * t < main_end) acc = __dadd_rn(acc, v[t]);
+            for (int t = 1; t < 16; t++) acc = __dadd_rn(acc, v[t]);  // pads add +0.0
             if (do_bracket) {
-                // fast path on the high words: "below bracket q" is exact
-                // unless hw == lo_hw[q]; anything within a bracket's
-                // high-word span is flagged for the exact path
+                // brackets are whole high-word ranges (host side), so the high
+                // word decides: d = hw - lo_hw, "below" is its sign (all high
+                // words < 2^31) and "inside" is d <= wid
+                npad += 16u - (uint32_t)nvalid;
                 uint32_t nearm = 0;
 #pragma unroll
                 for (int t = 0; t < 16; t++) {
                     const uint32_t hw = (uint32_t)(dbits(v[t]) >> 32);
-                    const bool have = j + 8 * t < main_end;
                     bool nr = false;
 #pragma unroll
                     for (int q = 0; q < NB; q++) {
-                        br.cnt[q] += (have && hw < br.lo_hw[q]) ? 1u : 0u;
-                        nr |= hw - br.lo_hw[q] <= br.wid_hw[q];
+                        const uint32_t d = hw - br.lo_hw[q];
+                        br.cnt[q] += d >> 31;
+                        nr |= d <= br.wid_hw[q];
                     }
-                    nearm |= (have && nr) ? (1u << t) : 0u;
+                    if (nr) nearm |= 1u << t;
                 }
-                // the rare near values: exact 64-bit classification (re-read
-                // from L1), count fix-up and candidate append
+                nearm &= (1u << nvalid) - 1u;  // a pad (+0.0) is inside a bracket starting at 0
+                // the (few) values inside a bracket, appended
                 while (__any_sync(0xffffffffu, nearm != 0)) {
-                    int list = -1;
+                    int ql = -1;
                     double w = 0.0;
                     if (nearm) {
                         const int t = __ffs(nearm) - 1;
                         nearm &= nearm - 1;
-                        w = __ldg(a + j + 8 * t);
-                        const uint64_t u = dbits(w);
-                        const uint32_t hw = (uint32_t)(u >> 32);
+                        w = pick16(v, t);
+                        const uint32_t hw = (uint32_t)(dbits(w) >> 32);
 #pragma unroll
-                        for (int q = 0; q < NB; q++) {
-                            br.cnt[q] += (hw == br.lo_hw[q] && u < br.lo[q]) ? 1u : 0u;
-                            if (u >= br.lo[q] && u <= br.hi[q]) list = (int)(g * MAX_LISTS + q);
-                        }
+                        for (int q = 0; q < NB; q++)
+                            if (hw - br.lo_hw[q] <= br.wid_hw[q]) ql = q;
                     }
-                    append(list, w, fill, off, cap, cand);
+                    push(ql, w);
                 }
             }
             // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) in numpy's order
@@ -310,11 +406,23 @@ __global__ void __launch_bounds__(LB_WARPS * 32) row_stats_kernel(
                 const double w = have ? a[idx] : 0.0;
                 if (have) res = __dadd_rn(res, w);
                 if (do_bracket) {
-                    const int q = classify_one<NB>(br, dbits(w), have);
-                    append(q >= 0 ? (int)(g * MAX_LISTS + q) : -1, w, fill, off, cap, cand);
+                    push(classify_one<NB>(br, dbits(w), have), w);
                 }
             }
             if (j == 0 && valid) lv[leaf] = res;  // leaves l0..l0+3 (lanes 0, 8, 16, 24)
+        };
+        double nv[16];
+        load_group(0, nv);
+        for (int l0 = 0; l0 < L; l0 += 4) {
+            double v[16];
+#pragma unroll
+            for (int t = 0; t < 16; t++) v[t] = nv[t];
+            load_group(l0 + 4, nv);
+            process_group(l0, v);
+        }
+        if (do_bracket) {
+#pragma unroll
+            for (int q = 0; q < NB; q++) br.cnt[q] -= ((0u - br.lo_hw[q]) >> 31) * npad;
         }
         // the split tree, one height at a time: nodes of equal height have
         // disjoint subtrees, so the lanes combine them in parallel
@@ -341,6 +449,8 @@ __global__ void __launch_bounds__(LB_WARPS * 32) row_stats_kernel(
                 for (int d = 16; d > 0; d >>= 1) c += __shfl_down_sync(0xffffffffu, c, d);
                 if (lane == 0 && q < nl && c) atomicAdd(&below[g * MAX_LISTS + q], (unsigned long long)c);
             }
+            cand_seal(cc, lane, nl, cap + gl0, off + gl0, cand);
+            if (lane < nl && cc.in) atomicAdd(&inside[gl0 + lane], (unsigned long long)cc.in);
         }
     }
 }
@@ -513,6 +623,7 @@ static int select_rows(const double* d_resp, int64_t n_groups, int64_t rows_per_
     cudaMemcpyAsync(h0, b_h0.p, b_h0.n, cudaMemcpyDeviceToHost, st);
     cudaMemcpyAsync(&bad, b_bad.p, sizeof(bad), cudaMemcpyDeviceToHost, st);
     if ((rc = check_cuda(cudaStreamSynchronize(st), "select hist sync"))) return rc;
+    trace("  sel hist0", st);
     if (bad) {
         set_error("cs_rep_stats: %llu negative responses (impossible for valid input)", bad);
         return CS_INTERNAL;
@@ -555,8 +666,9 @@ static int select_rows(const double* d_resp, int64_t n_groups, int64_t rows_per_
                 list = nlist[g]++;
                 bucket[g * SEL_LISTS + list] = b;
                 off[g * SEL_LISTS + list] = total;
-                cap[g * SEL_LISTS + list] = hg[b];
-                total += hg[b];
+                // + the reserved-but-unused slots: < 2 chunks per row
+                cap[g * SEL_LISTS + list] = hg[b] + 2 * CAND_CHUNK * rows_per_group;
+                total += cap[g * SEL_LISTS + list];
             }
             SelSlot& s = slots[g * n_ranks + q];
             s.prefix = (uint64_t)b << 48;
@@ -565,6 +677,7 @@ static int select_rows(const double* d_resp, int64_t n_groups, int64_t rows_per_
             s.cand_len = cap[g * SEL_LISTS + list];
         }
     }
+    trace("  sel buckets", st);
     DBuf b_nl, b_bk, b_off, b_cap, b_fill, b_cand;
     if ((rc = b_nl.alloc(sizeof(int32_t) * n_groups, st)) ||
         (rc = b_bk.alloc(sizeof(uint32_t) * SEL_LISTS * n_groups, st)) ||
@@ -578,21 +691,12 @@ static int select_rows(const double* d_resp, int64_t n_groups, int64_t rows_per_
     cudaMemcpyAsync(b_off.p, off.data(), b_off.n, cudaMemcpyHostToDevice, st);
     cudaMemcpyAsync(b_cap.p, cap.data(), b_cap.n, cudaMemcpyHostToDevice, st);
     cudaMemsetAsync(b_fill.p, 0, b_fill.n, st);
-    compact_bucket_kernel<<<(unsigned)std::min<int64_t>(n_rows, (int64_t)sm_count() * 16), 256, 0, st>>>(
+    cudaMemsetAsync(b_cand.p, 0xff, b_cand.n, st);  // CAND_SENTINEL
+    compact_bucket_kernel<<<(unsigned)std::min<int64_t>((n_rows + 7) / 8, (int64_t)sm_count() * 16), 256, 0, st>>>(
         d_resp, n_rows, rv, ldr, rows_per_group, b_nl.as<int32_t>(), b_bk.as<uint32_t>(), b_off.as<int64_t>(),
         b_cap.as<int64_t>(), b_fill.as<unsigned long long>(), b_cand.as<double>());
     if ((rc = check_launch("compact_bucket_kernel"))) return rc;
-    if (dist) {  // candidates are this rank's values only: use the local counts
-        std::vector<unsigned long long> fill((size_t)SEL_LISTS * n_groups);
-        cudaMemcpyAsync(fill.data(), b_fill.p, b_fill.n, cudaMemcpyDeviceToHost, st);
-        if ((rc = check_cuda(cudaStreamSynchronize(st), "compact sync"))) return rc;
-        for (int64_t g = 0; g < n_groups; g++)
-            for (int q = 0; q < n_ranks; q++) {
-                SelSlot& s = slots[g * n_ranks + q];
-                for (int l = 0; l < nlist[g]; l++)
-                    if (off[g * SEL_LISTS + l] == s.cand_off) s.cand_len = (int64_t)fill[g * SEL_LISTS + l];
-            }
-    }
+    trace("  sel compact", st);
     if ((rc = run_rounds(slots, b_cand.as<double>(), 36, dist, st))) return rc;  // bits 47..0
     out.resize(slots.size());
     for (size_t i = 0; i < slots.size(); i++) memcpy(&out[i], &slots[i].prefix, 8);
@@ -709,15 +813,15 @@ extern "C" int cs_rep_stats_impl(const double* d_resp, int32_t n_groups, int64_t
     int max_brackets = 0;  // set per bracket attempt; selects the kernel instance
     auto leaf_pass = [&](int do_bracket, const int32_t* nl, const uint64_t* lo, const uint64_t* hi,
                          const int64_t* off, const int64_t* cap, unsigned long long* fill,
-                         unsigned long long* below, double* cand) {
+                         unsigned long long* below, unsigned long long* inside, double* cand) {
         if (max_brackets <= 3)
             row_stats_kernel<3><<<blocks, LB_WARPS * 32, std::max<size_t>(smem, 16), st>>>(
                 d_resp, n_rows, rows_per_group, ldr, m, b_plan.as<int32_t>(), L, d_summ, d_row_sums, do_bracket,
-                nl, lo, hi, off, cap, fill, below, cand, n_heights, leaf_scratch);
+                nl, lo, hi, off, cap, fill, below, inside, cand, n_heights, leaf_scratch);
         else
             row_stats_kernel<MAX_LISTS><<<blocks, LB_WARPS * 32, std::max<size_t>(smem, 16), st>>>(
                 d_resp, n_rows, rows_per_group, ldr, m, b_plan.as<int32_t>(), L, d_summ, d_row_sums, do_bracket,
-                nl, lo, hi, off, cap, fill, below, cand, n_heights, leaf_scratch);
+                nl, lo, hi, off, cap, fill, below, inside, cand, n_heights, leaf_scratch);
         return check_launch("row_stats_kernel");
     };
     auto combine = [&]() { return CS_OK; };  // the tree is combined on chip
@@ -728,7 +832,7 @@ extern "C" int cs_rep_stats_impl(const double* d_resp, int32_t n_groups, int64_t
     const int64_t n_chunks = m / 128, tail = std::min<int64_t>(4, m % 128);
     const RowView sample{n_chunks * 4 + tail, 2, 7};
     if (!want_ranks || N <= (1 << 20) || sample.len < 64) {
-        if ((rc = leaf_pass(0, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr)) ||
+        if ((rc = leaf_pass(0, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr)) ||
             (rc = combine()))
             return rc;
         if (!want_ranks) return CS_OK;
@@ -778,9 +882,13 @@ extern "C" int cs_rep_stats_impl(const double* d_resp, int32_t n_groups, int64_t
         for (int64_t g = 0; g < n_groups; g++) {
             std::vector<int> idx(n_ranks);
             for (int q = 0; q < n_ranks; q++) idx[q] = q;
-            auto a_of = [&](int q) { return r_lo[g * n_ranks + q] == 0 ? 0ull : bits_of(v_lo[g * n_ranks + q]); };
+            // whole high-word ranges: the row pass classifies on the high 32 bits alone
+            auto a_of = [&](int q) {
+                return r_lo[g * n_ranks + q] == 0 ? 0ull : bits_of(v_lo[g * n_ranks + q]) & ~0xffffffffull;
+            };
             auto b_of = [&](int q) {
-                return r_hi[g * n_ranks + q] == NS - 1 ? 0x7fffffffffffffffull : bits_of(v_hi[g * n_ranks + q]);
+                return r_hi[g * n_ranks + q] == NS - 1 ? 0x7fffffffffffffffull
+                                                       : bits_of(v_hi[g * n_ranks + q]) | 0xffffffffull;
             };
             std::sort(idx.begin(), idx.end(), [&](int x, int y) { return a_of(x) < a_of(y); });
             for (int q : idx) {
@@ -803,7 +911,9 @@ extern "C" int cs_rep_stats_impl(const double* d_resp, int32_t n_groups, int64_t
         for (int64_t g = 0; g < n_groups; g++)
             for (int l = 0; l < nlist[g]; l++) {
                 const double scale = (double)N / (double)NS;
-                const int64_t c = std::min<int64_t>(N, (int64_t)(4.0 * est[g * MAX_LISTS + l] * scale) + 4096);
+                // + the reserved-but-unused slots: < 2 chunks per row and list
+                const int64_t c = std::min<int64_t>(N, (int64_t)(4.0 * est[g * MAX_LISTS + l] * scale) + 4096) +
+                                  2 * CAND_CHUNK * rows_per_group;
                 off[g * MAX_LISTS + l] = total;
                 cap[g * MAX_LISTS + l] = c;
                 total += c;
@@ -811,10 +921,10 @@ extern "C" int cs_rep_stats_impl(const double* d_resp, int32_t n_groups, int64_t
                 if (d) top_bit = std::max(top_bit, 63 - __builtin_clzll(d));
             }
         // ---- 2. the one full pass: leaf sums + bracket counts/compaction ----
-        DBuf b_nl, b_lo, b_hi, b_off, b_cap, b_fill, b_below, b_cand;
+        DBuf b_nl, b_lo, b_hi, b_off, b_cap, b_fill, b_below, b_inside, b_cand;
         if ((rc = b_nl.alloc(sizeof(int32_t) * n_groups, st)) || (rc = b_lo.alloc(8 * L6, st)) ||
             (rc = b_hi.alloc(8 * L6, st)) || (rc = b_off.alloc(8 * L6, st)) || (rc = b_cap.alloc(8 * L6, st)) ||
-            (rc = b_fill.alloc(8 * L6, st)) || (rc = b_below.alloc(8 * L6, st)) ||
+            (rc = b_fill.alloc(8 * L6, st)) || (rc = b_below.alloc(8 * L6, st)) || (rc = b_inside.alloc(8 * L6, st)) ||
             (rc = b_cand.alloc(sizeof(double) * std::max<int64_t>(total, 1), st)))
             return rc;
         cudaMemcpyAsync(b_nl.p, nlist.data(), b_nl.n, cudaMemcpyHostToDevice, st);
@@ -824,17 +934,20 @@ extern "C" int cs_rep_stats_impl(const double* d_resp, int32_t n_groups, int64_t
         cudaMemcpyAsync(b_cap.p, cap.data(), b_cap.n, cudaMemcpyHostToDevice, st);
         cudaMemsetAsync(b_fill.p, 0, b_fill.n, st);
         cudaMemsetAsync(b_below.p, 0, b_below.n, st);
+        cudaMemsetAsync(b_inside.p, 0, b_inside.n, st);
         max_brackets = *std::max_element(nlist.begin(), nlist.end());
         trace("bracket setup", st);
         if ((rc = leaf_pass(1, b_nl.as<int32_t>(), b_lo.as<uint64_t>(), b_hi.as<uint64_t>(), b_off.as<int64_t>(),
-                            b_cap.as<int64_t>(), b_fill.as<unsigned long long>(), b_below.as<unsigned long long>(),
+                            b_cap.as<int64_t>(), b_fill.as<unsigned long long>(), b_below.as<unsigned long long>(), b_inside.as<unsigned long long>(),
                             b_cand.as<double>())))
             return rc;
         if (!combined) {
             if ((rc = combine())) return rc;
             combined = true;
         }
-        std::vector<unsigned long long> fill(L6), below(L6), fill_all(L6), overflow(L6);
+        // fill = reserved slots (the candidate lists' lengths, sealed tails
+        // included); inside = values actually inside the brackets
+        std::vector<unsigned long long> fill(L6), below(L6), inside_all(L6), overflow(L6);
         cudaMemcpyAsync(fill.data(), b_fill.p, b_fill.n, cudaMemcpyDeviceToHost, st);
         if ((rc = check_cuda(cudaStreamSynchronize(st), "bracket sync"))) return rc;
         for (size_t li = 0; li < L6; li++) overflow[li] = (int64_t)fill[li] > cap[li] ? 1 : 0;
@@ -842,12 +955,12 @@ extern "C" int cs_rep_stats_impl(const double* d_resp, int32_t n_groups, int64_t
             DBuf b_ov;
             if ((rc = b_ov.alloc(8 * L6, st))) return rc;
             cudaMemcpyAsync(b_ov.p, overflow.data(), 8 * L6, cudaMemcpyHostToDevice, st);
-            if ((rc = allreduce_u64(b_below.p, L6, st)) || (rc = allreduce_u64(b_fill.p, L6, st)) ||
+            if ((rc = allreduce_u64(b_below.p, L6, st)) || (rc = allreduce_u64(b_inside.p, L6, st)) ||
                 (rc = allreduce_max_u64(b_ov.p, L6, st)))
                 return rc;
             cudaMemcpyAsync(overflow.data(), b_ov.p, 8 * L6, cudaMemcpyDeviceToHost, st);
         }
-        cudaMemcpyAsync(fill_all.data(), b_fill.p, b_fill.n, cudaMemcpyDeviceToHost, st);
+        cudaMemcpyAsync(inside_all.data(), b_inside.p, b_inside.n, cudaMemcpyDeviceToHost, st);
         cudaMemcpyAsync(below.data(), b_below.p, b_below.n, cudaMemcpyDeviceToHost, st);
         if ((rc = check_cuda(cudaStreamSynchronize(st), "bracket sync 2"))) return rc;
         trace("row pass+counts", st);
@@ -860,11 +973,11 @@ extern "C" int cs_rep_stats_impl(const double* d_resp, int32_t n_groups, int64_t
             const int64_t g = (int64_t)i / n_ranks;
             const size_t li = g * MAX_LISTS + list_of[i];
             const int64_t k = target[i];
-            if (overflow[li] || (int64_t)below[li] > k || k >= (int64_t)(below[li] + fill_all[li])) {
+            if (overflow[li] || (int64_t)below[li] > k || k >= (int64_t)(below[li] + inside_all[li])) {
                 if (getenv("CS_DEBUG_STATS"))
                     fprintf(stderr, "[cs_rep_stats] bracket miss: attempt %d slot %zu k=%lld below=%llu "
                             "fill=%llu local=%llu cap=%lld ovf=%llu lo=%016llx hi=%016llx dist=%d\n",
-                            attempt, i, (long long)k, below[li], fill_all[li], fill[li], (long long)cap[li],
+                            attempt, i, (long long)k, below[li], inside_all[li], fill[li], (long long)cap[li],
                             overflow[li], (unsigned long long)lo[li], (unsigned long long)hi[li], (int)dist);
                 ok = false;
                 break;
