@@ -138,7 +138,14 @@ class SweepEngine:
         torch = self.torch
         if len(self.sets) < 2:
             self.sets.append(self._alloc_set())
-            self.pipe = [torch.cuda.Stream() for _ in range(3)]
+            # the simulator's stream has the higher priority: when sweep k-1
+            # ends, sweep k's blocks (resident for the whole sweep) must be
+            # spread over all SMs before the statistics of sweep k-1 take any
+            # -- blocks placed on the few SMs the statistics left free would
+            # pile up there and stretch the simulation several-fold
+            # (lower number = higher priority; torch clamps to the device's range)
+            self.pipe = [torch.cuda.Stream(priority=0), torch.cuda.Stream(priority=-8),
+                         torch.cuda.Stream(priority=0)]
         s_gen, s_sim, s_stat = self.pipe
         cur = torch.cuda.current_stream()
         for s_ in self.pipe:
