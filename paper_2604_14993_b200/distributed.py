@@ -24,7 +24,7 @@ from typing import Sequence
 import numpy as np
 
 from . import _native as N
-from .sim import SimConfig, SimStats, _require_supported, _stats_from
+from .sim import SimConfig, SimStats, _require_supported, _stats_from_batch
 
 _initialised = False
 
@@ -106,4 +106,4 @@ def run_sim_sharded(configs: Sequence[SimConfig]) -> list[SimStats]:
     summ = all_gather_rows(eng.summaries())                       # [P, R]
     busy = all_gather_rows(eng.busy())                            # [P, R, ldb]
     order = eng.order_stats()
-    return [_stats_from(c, summ[p], busy[p], order[p], None) for p, c in enumerate(configs)]
+    return _stats_from_batch(configs, summ, busy, order, None)

@@ -211,58 +211,112 @@ def _require_supported(cfg: SimConfig) -> None:
                          "use run_sim for other policies and workloads")
 
 
+def _rows_nanmean(x: np.ndarray) -> np.ndarray:
+    """_nanmean of every row of a [P, R] array (row means are numpy's pairwise
+    sums of the contiguous rows, as for the 1-D finite copy)."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    nan = np.isnan(x)
+    out = x.mean(axis=1) if x.shape[1] else np.full(x.shape[0], math.nan)
+    for p in np.flatnonzero(nan.any(axis=1)):
+        out[p] = _nanmean(x[p])
+    return out
+
+
+def _rows_ci_half_width(x: np.ndarray) -> np.ndarray:
+    """_ci_half_width of every row (x.std(ddof=1) reduces each contiguous row
+    exactly as the 1-D call does)."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    P, R = x.shape
+    if R < 2:
+        return np.full(P, math.nan)
+    out = _t975(R - 1) * x.std(axis=1, ddof=1) / math.sqrt(R)
+    out[np.isnan(x).any(axis=1)] = math.nan
+    return out
+
+
 def _stats_from(cfg: SimConfig, summ: np.ndarray, busy: np.ndarray, order_stats: dict,
                 jobs: np.ndarray | None) -> SimStats:
-    """sim.py:406-456 on per-replication summaries (no response re-reads on host)."""
-    R = cfg.replications
-    if np.any(summ["counted"] < 0):  # jffc_sim_k1_kernel merge-feed overflow (never seen)
+    """sim.py:406-456 on one point's per-replication summaries."""
+    return _stats_from_batch([cfg], summ[None], busy[None], [order_stats],
+                             None if jobs is None else jobs[None])[0]
+
+
+def _stats_from_batch(configs: Sequence[SimConfig], summ: np.ndarray, busy: np.ndarray,
+                      order_stats: Sequence[dict], jobs: np.ndarray | None) -> list[SimStats]:
+    """sim.py:406-456 for P points at once ([P, R] summaries, [P, R, ldb] busy
+    times): the per-point reductions run row-wise over contiguous copies of
+    the summary fields, each row reduced exactly as the reference reduces
+    that point's list (no response re-reads on host)."""
+    R = configs[0].replications
+    summ = summ[:, :R]
+    # every field is 8 bytes: one transposing copy gives each field as a
+    # contiguous [P, R] array
+    names = summ.dtype.names
+    planes = np.ascontiguousarray(
+        np.ascontiguousarray(summ).view(np.float64).reshape(summ.shape + (len(names),)).transpose(2, 0, 1))
+    col = {f: planes[i].view(summ.dtype[f]) for i, f in enumerate(names)}
+    if np.any(col["counted"] < 0):  # jffc_sim_k1_kernel merge-feed overflow (never seen)
         raise AssertionError("simulation merge feed overflowed (exact finish-time ties)")
-    counted = int(summ["counted"].sum())
-    rep_means = tuple(summ["resp_mean"].tolist())
-    rep_occ = tuple(summ["mean_occupancy"].tolist())
+    counted = col["counted"].sum(axis=1)
+    rep_means = col["resp_mean"].tolist()
+    rep_occ = col["mean_occupancy"].tolist()
+    resp_sums = col["resp_sum"].tolist()
     # sim.py:410-411 sums np.float64 values, so builtin sum() is the naive
-    # left-to-right sum there (CPython compensates exact floats only)
-    total_wait = _naive_sum(summ["wait_sum"])
-    total_service = _naive_sum(summ["service_sum"])
-    occ_a = np.asarray(summ["mean_occupancy"], dtype=np.float64)
-    mean_occ = _nanmean(occ_a)
-    lam_eff = _nanmean(summ["lambda_effective"])
-    # merged.mean(): correctly rounded sum of the per-rep pairwise sums
-    mean_resp = math.fsum(summ["resp_sum"].tolist()) / counted
-    caps = cfg.capacities
-    windows = np.asarray(summ["window_s"], dtype=np.float64)
+    # left-to-right sum there (CPython compensates exact floats only);
+    # np.add.accumulate runs left to right along each row
+    total_wait = np.add.accumulate(col["wait_sum"], axis=1)[:, -1] if R else np.zeros(len(configs))
+    total_service = np.add.accumulate(col["service_sum"], axis=1)[:, -1] if R else np.zeros(len(configs))
+    mean_occ = _rows_nanmean(col["mean_occupancy"])
+    lam_eff = _rows_nanmean(col["lambda_effective"])
+    occ_h1 = _rows_nanmean(col["occ_first_half"])
+    occ_h2 = _rows_nanmean(col["occ_second_half"])
+    resp_ci = _rows_ci_half_width(col["resp_mean"])
+    occ_ci = _rows_ci_half_width(col["mean_occupancy"])
+    # per-chain utilisation: busy / (c_k * window) where window > 0, row nanmeans
+    windows = col["window_s"]
+    K = max(len(c.capacities) for c in configs)
+    caps_pk = np.ones((len(configs), K), np.float64)
+    for p, c in enumerate(configs):
+        caps_pk[p, :len(c.capacities)] = c.capacities
     with np.errstate(divide="ignore", invalid="ignore"):  # same IEEE ops, element-wise
-        util = tuple(
-            _nanmean(np.where(windows > 0, np.asarray(busy[:R, k], np.float64) / (caps[k] * windows),
-                              math.nan))
-            for k in range(len(caps)))
-    little = (abs(mean_occ - lam_eff * mean_resp) / mean_occ
-              if mean_occ and not math.isnan(mean_occ) else math.nan)
-    qv = {}
-    for q in QUANTILES:
-        prev, nxt, gamma = _quantile_ranks(counted, q)
-        qv[q] = _lerp(order_stats[prev], order_stats[nxt], gamma)
-    records = None
-    if cfg.collect_jobs and jobs is not None:
-        records = tuple((r, float(a), float(s), float(f), int(k))
-                        for r in range(R) for a, s, f, k in jobs[r])
-    # sim.py:442,452: offered load is the Poisson rate, else the measured one
-    offered = cfg.workload.rate if isinstance(cfg.workload, PoissonWorkload) or (
-        hasattr(cfg.workload, "rate") and not hasattr(cfg.workload, "sizes")) else lam_eff
-    unstable = bool(offered >= cfg.total_rate) if not math.isnan(offered) else False
-    return SimStats(
-        policy=cfg.policy, jobs_counted=counted, mean_response_s=mean_resp,
-        median_response_s=qv[0.5], p95_response_s=qv[0.95], p99_response_s=qv[0.99],
-        mean_waiting_s=total_wait / counted, mean_service_s=total_service / counted,
-        mean_occupancy=mean_occ,
-        response_ci_half_width_s=_ci_half_width(np.asarray(summ["resp_mean"], dtype=np.float64)),
-        occupancy_ci_half_width=_ci_half_width(occ_a), per_chain_utilization=util,
-        lambda_effective=lam_eff, little_law_gap=little,
-        unstable=unstable, seed=cfg.seed, replications=R,
-        rep_mean_response_s=rep_means, rep_mean_occupancy=rep_occ,
-        occ_first_half=_nanmean(summ["occ_first_half"]),
-        occ_second_half=_nanmean(summ["occ_second_half"]),
-        end_queue_len=int(summ["end_queue_len"].max()), job_records=records)
+        ratio = np.where(windows[:, None, :] > 0,
+                         np.asarray(busy[:, :R, :K], np.float64).transpose(0, 2, 1)
+                         / (caps_pk[:, :, None] * windows[:, None, :]), math.nan)
+    util_all = _rows_nanmean(ratio.reshape(-1, R)).reshape(len(configs), K)
+    end_q = col["end_queue_len"].max(axis=1) if R else np.zeros(len(configs), np.int64)
+    out = []
+    for p, cfg in enumerate(configs):
+        n_counted = int(counted[p])
+        # merged.mean(): correctly rounded sum of the per-rep pairwise sums
+        mean_resp = math.fsum(resp_sums[p]) / n_counted
+        util = tuple(float(v) for v in util_all[p, :len(cfg.capacities)])
+        mo, le = float(mean_occ[p]), float(lam_eff[p])
+        little = (abs(mo - le * mean_resp) / mo if mo and not math.isnan(mo) else math.nan)
+        qv = {}
+        for q in QUANTILES:
+            prev, nxt, gamma = _quantile_ranks(n_counted, q)
+            qv[q] = _lerp(order_stats[p][prev], order_stats[p][nxt], gamma)
+        records = None
+        if cfg.collect_jobs and jobs is not None:
+            records = tuple((r, float(a), float(s), float(f), int(k))
+                            for r in range(R) for a, s, f, k in jobs[p][r])
+        # sim.py:442,452: offered load is the Poisson rate, else the measured one
+        offered = cfg.workload.rate if isinstance(cfg.workload, PoissonWorkload) or (
+            hasattr(cfg.workload, "rate") and not hasattr(cfg.workload, "sizes")) else le
+        unstable = bool(offered >= cfg.total_rate) if not math.isnan(offered) else False
+        out.append(SimStats(
+            policy=cfg.policy, jobs_counted=n_counted, mean_response_s=mean_resp,
+            median_response_s=qv[0.5], p95_response_s=qv[0.95], p99_response_s=qv[0.99],
+            mean_waiting_s=float(total_wait[p]) / n_counted,
+            mean_service_s=float(total_service[p]) / n_counted,
+            mean_occupancy=mo, response_ci_half_width_s=float(resp_ci[p]),
+            occupancy_ci_half_width=float(occ_ci[p]), per_chain_utilization=util,
+            lambda_effective=le, little_law_gap=little,
+            unstable=unstable, seed=cfg.seed, replications=R,
+            rep_mean_response_s=tuple(rep_means[p]), rep_mean_occupancy=tuple(rep_occ[p]),
+            occ_first_half=float(occ_h1[p]), occ_second_half=float(occ_h2[p]),
+            end_queue_len=int(end_q[p]), job_records=records))
+    return out
 
 
 @dataclass
@@ -338,9 +392,7 @@ def run_sim_batch(configs: Sequence[SimConfig]) -> list[SimStats]:
     res = simulate_sweep([c.rates for c in configs], [c.capacities for c in configs],
                          [c.workload.rate for c in configs], c0.horizon_jobs, c0.warmup_fraction,
                          c0.seed, c0.replications, collect_jobs=c0.collect_jobs)
-    return [_stats_from(c, res.summaries[p], res.busy[p], res.order_stats[p],
-                        res.jobs[p] if res.jobs is not None else None)
-            for p, c in enumerate(configs)]
+    return _stats_from_batch(configs, res.summaries, res.busy, res.order_stats, res.jobs)
 
 
 def run_sim(config: SimConfig) -> SimStats:

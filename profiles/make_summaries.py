@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Turn a round's raw ncu outputs (gpurun_out/, scratch) into the committed
 summaries under profiles/.  Inputs, all from one gpurun call of
-scratch/profile_round.sh (same bench command, N=1, config 2):
+profiles/profile_round.sh (same bench command, N=1, config 2):
 
   prof_launches.csv  ncu --metrics gpu__time_duration.sum (every launch of
                      `bench.py --steps 2 --warmup 3`, cold-cache, serialised)
