@@ -124,3 +124,49 @@ def test_chainrates():
     assert cr.total_capacity == 6 and cr.total_rate == 13.0
     with pytest.raises(ValueError):
         P.ChainRates((1.0, 2.0), (1, 1))
+
+
+def test_batched_aggregation_matches_per_point_numpy():
+    """_stats_from_batch reduces each point's row exactly as numpy reduces that
+    point's 1-D arrays (sim.py:406-456): compare against direct 1-D numpy on
+    random summaries with NaNs, several replication counts and chain counts."""
+    from paper_2604_14993_b200 import _native as N
+
+    rng = np.random.default_rng(5)
+
+    def bits_equal(a, b):
+        return (math.isnan(a) and math.isnan(b)) or np.float64(a).tobytes() == np.float64(b).tobytes()
+
+    class Order(dict):
+        def __missing__(self, k):
+            return 1.0 + k * 1e-9
+
+    for R in (1, 2, 7, 129, 1024):
+        Pn, K = 3, 2
+        summ = np.zeros((Pn, R), N.SUMMARY_DTYPE)
+        for f in summ.dtype.names:
+            summ[f] = (rng.uniform(0.1, 50, (Pn, R)) if summ.dtype[f].kind == "f"
+                       else rng.integers(1, 90000, (Pn, R)))
+        summ["mean_occupancy"][rng.random((Pn, R)) < 0.05] = np.nan
+        busy = rng.uniform(0, 5, (Pn, R, K))
+        cfgs = [P.SimConfig(rates=(0.5, 0.25), capacities=(2, 3), workload=P.PoissonWorkload(0.2),
+                            horizon_jobs=1000, warmup_fraction=0.1, seed=1, replications=R)
+                for _ in range(Pn)]
+        out = S._stats_from_batch(cfgs, summ, busy, [Order() for _ in range(Pn)], None)
+        for p in range(Pn):
+            occ = np.array(summ["mean_occupancy"][p])
+            fin = occ[~np.isnan(occ)]
+            assert bits_equal(out[p].mean_occupancy, float(fin.mean()) if fin.size else math.nan)
+            rm = np.array(summ["resp_mean"][p])
+            ci = (math.nan if R < 2 else float(S._t975(R - 1) * rm.std(ddof=1) / math.sqrt(R)))
+            assert bits_equal(out[p].response_ci_half_width_s, ci)
+            w = np.array(summ["window_s"][p])
+            for k in range(K):
+                u = np.where(w > 0, np.array(busy[p, :, k]) / (cfgs[p].capacities[k] * w), math.nan)
+                fu = u[~np.isnan(u)]
+                assert bits_equal(out[p].per_chain_utilization[k], float(fu.mean()) if fu.size else math.nan)
+            ws = 0.0
+            for x in summ["wait_sum"][p]:
+                ws += x
+            assert bits_equal(out[p].mean_waiting_s, float(ws) / int(summ["counted"][p].sum()))
+            assert out[p].rep_mean_response_s == tuple(summ["resp_mean"][p].tolist())
