@@ -167,19 +167,22 @@ class SweepEngine:
         if steps > 0:
             gen(0)
         if self.distributed and not os.environ.get("CS_PIPE_DIST_OVERLAP"):
-            # sharded: every stage in one stream's order.  The statistics'
-            # NCCL collectives cannot run beside the simulator (their kernels
-            # need an SM configuration the simulator's SMs do not offer), and
-            # overlapping only the next sweep's streams with the simulation
-            # measured 56-71 ms per sweep at N=4 against 45 ms in order
-            # (the streams' blocks, placed first, unbalance the simulator's)
+            # sharded: the statistics' NCCL collectives cannot run beside the
+            # simulator (their kernels need an SM configuration the simulator's
+            # SMs do not offer), so they follow each simulation in its stream;
+            # the next sweep's streams run beside these statistics, not beside
+            # the simulation (overlapping the simulation measured 56-71 ms per
+            # sweep at N=4 against 45 ms: the streams' blocks, placed first,
+            # unbalance the simulator's)
             for k in range(steps):
                 b = k & 1
-                if k > 0:
-                    self.streams(b, s_sim)
-                else:
-                    s_sim.wait_event(ev_gen[b])
+                s_sim.wait_event(ev_gen[b])
                 self.simulate(b, s_sim)
+                ev_sim[b].record(s_sim)
+                if k + 1 < steps:
+                    s_gen.wait_event(ev_sim[b])
+                    self.streams((k + 1) & 1, s_gen)
+                    ev_gen[(k + 1) & 1].record(s_gen)
                 self.statistics(b, s_sim)
                 if after_stats is not None:
                     after_stats(b, s_sim)
