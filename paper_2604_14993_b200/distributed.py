@@ -82,6 +82,23 @@ def all_gather_rows(local: np.ndarray) -> np.ndarray:
     return np.concatenate(parts, axis=1 if local.ndim >= 2 else 0)
 
 
+def _gather_device_rows(dev, dtype, shape) -> np.ndarray:
+    """Every rank's device array of `shape` ([P, R, ...], point-major) gathered
+    in rank order along the replication axis: one NCCL all-gather straight
+    from the device buffer and one read-back."""
+    import torch
+    import torch.distributed as dist
+
+    rank, world = rank_world()
+    if world == 1:
+        return dev.cpu().numpy().view(dtype).reshape(shape).copy()
+    flat = dev.reshape(-1)
+    out = torch.empty(world * flat.numel(), dtype=flat.dtype, device=flat.device)
+    dist.all_gather_into_tensor(out, flat)
+    parts = out.cpu().numpy().view(dtype).reshape((world,) + tuple(shape))
+    return np.concatenate(list(parts), axis=1)
+
+
 def run_sim_sharded(configs: Sequence[SimConfig]) -> list[SimStats]:
     """run_sim_batch with the replications of every config split over the ranks."""
     from .engine import SweepEngine
@@ -103,7 +120,7 @@ def run_sim_sharded(configs: Sequence[SimConfig]) -> list[SimStats]:
                       c0.seed, count, rep_begin=begin, distributed=world > 1,
                       total_reps=c0.replications)
     eng.step()
-    summ = all_gather_rows(eng.summaries())                       # [P, R]
-    busy = all_gather_rows(eng.busy())                            # [P, R, ldb]
+    summ = _gather_device_rows(eng.sets[0]["summ"], N.SUMMARY_DTYPE, (eng.P, eng.R))   # [P, R]
+    busy = _gather_device_rows(eng.sets[0]["busy"], np.float64, (eng.P, eng.R, eng.ldb))
     order = eng.order_stats()
     return _stats_from_batch(configs, summ, busy, order, None)
