@@ -153,14 +153,10 @@ class SweepEngine:
         ev_sim = [torch.cuda.Event(), torch.cuda.Event()]
         ev_stat = [torch.cuda.Event(), torch.cuda.Event()]
         ev_gen = [torch.cuda.Event(), torch.cuda.Event()]
-        ev_go = torch.cuda.Event()  # the simulator's stream reached the next simulation
         def gen(k):  # streams of sweep k into set k & 1 (free once sweep k-2 simulated)
             b = k & 1
             if k >= 2:
                 s_gen.wait_event(ev_sim[b])
-                # not before the running sweep's simulation is ready to start:
-                # its blocks must be placed first (see the priorities above)
-                s_gen.wait_event(ev_go)
             self.streams(b, s_gen)
             ev_gen[b].record(s_gen)
 
@@ -195,7 +191,6 @@ class SweepEngine:
                 s_sim.wait_event(ev_gen[b])
                 if k >= 2:
                     s_sim.wait_event(ev_stat[b])  # response buffer b read by sweep k-2
-                ev_go.record(s_sim)
                 self.simulate(b, s_sim)
                 ev_sim[b].record(s_sim)
                 if k + 1 < steps:  # enqueued before the (host-blocking) statistics below
