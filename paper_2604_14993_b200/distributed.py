@@ -66,22 +66,6 @@ def init() -> None:
     _initialised = True
 
 
-def all_gather_rows(local: np.ndarray) -> np.ndarray:
-    """Concatenate equal-shape per-rank arrays in rank order (NCCL all-gather)."""
-    import torch
-    import torch.distributed as dist
-
-    rank, world = rank_world()
-    if world == 1:
-        return local
-    flat = np.ascontiguousarray(local).view(np.uint8).ravel()
-    t = torch.from_numpy(flat).to("cuda")
-    out = [torch.empty_like(t) for _ in range(world)]
-    dist.all_gather(out, t)
-    parts = [o.cpu().numpy().view(local.dtype).reshape(local.shape) for o in out]
-    return np.concatenate(parts, axis=1 if local.ndim >= 2 else 0)
-
-
 def _gather_device_rows(dev, dtype, shape) -> np.ndarray:
     """Every rank's device array of `shape` ([P, R, ...], point-major) gathered
     in rank order along the replication axis: one NCCL all-gather straight

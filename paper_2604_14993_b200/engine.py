@@ -11,7 +11,6 @@ stream; all compute is the engine's own kernels via the C-ABI.
 from __future__ import annotations
 
 import ctypes as C
-import os
 from dataclasses import dataclass
 from typing import Sequence
 
@@ -162,7 +161,7 @@ class SweepEngine:
 
         if steps > 0:
             gen(0)
-        if self.distributed and not os.environ.get("CS_PIPE_DIST_OVERLAP"):
+        if self.distributed:
             # sharded: the statistics' NCCL collectives cannot run beside the
             # simulator (their kernels need an SM configuration the simulator's
             # SMs do not offer), so they follow each simulation in its stream;
