@@ -236,11 +236,14 @@ __global__ void __launch_bounds__(256) compact_bucket_kernel(
     }
 }
 
-// v[t] for a runtime t without local memory: a 4-level select tree
-__device__ __forceinline__ double pick16(const double (&v)[16], int t) {
+// v[t] for a runtime t < T without local memory: a select tree over the
+// bits of t (levels of a power-of-two padding; slots >= T never chosen)
+template <int T>
+__device__ __forceinline__ double pick_slot(const double (&v)[T], int t) {
     double l1[8], l2[4], l3[2];
 #pragma unroll
-    for (int i = 0; i < 8; i++) l1[i] = (t & 1) ? v[2 * i + 1] : v[2 * i];
+    for (int i = 0; i < 8; i++)
+        l1[i] = (t & 1) ? v[2 * i + 1 < T ? 2 * i + 1 : T - 1] : v[2 * i < T ? 2 * i : T - 1];
 #pragma unroll
     for (int i = 0; i < 4; i++) l2[i] = (t & 2) ? l1[2 * i + 1] : l1[2 * i];
 #pragma unroll
@@ -285,7 +288,10 @@ __device__ __forceinline__ int classify_one(Brackets<NB>& br, uint64_t u, bool h
 // height-ordered nodes) sits in shared memory.
 constexpr int LB_WARPS = 8;
 
-template <int NB>
+// T = value slots per lane and leaf: 8*T >= the plan's longest leaf (numpy
+// leaves hold 64..128 values; 90000-value rows have 80/88-value leaves, so
+// T = 12 there instead of 16 saves a quarter of the per-slot work)
+template <int NB, int T>
 __global__ void __launch_bounds__(LB_WARPS * 32, 2) row_stats_kernel(
     const double* __restrict__ resp, int64_t n_rows, int64_t rows_per_group, int64_t ldr, int64_t m,
     const int32_t* __restrict__ g_plan, int32_t L, cs_rep_summary* __restrict__ summ,
@@ -339,15 +345,15 @@ __global__ void __launch_bounds__(LB_WARPS * 32, 2) row_stats_kernel(
         // sums unchanged (all values are >= +0) and is counted "below" by the
         // fast path exactly when 0 < lo_hw; that is undone per lane at the end.
         uint32_t npad = 0;
-        auto load_group = [&](int leaf0, double (&buf)[16]) {
+        auto load_group = [&](int leaf0, double (&buf)[T]) {
             const int leaf = leaf0 + sub;
             const int len = leaf < L ? leaf_len[leaf] : 0;
             const double* __restrict__ a = rowp + (leaf < L ? leaf_off[leaf] : 0);
             const int main_end = len >= 8 ? len - len % 8 : 0;
 #pragma unroll
-            for (int t = 0; t < 16; t++) buf[t] = (j + 8 * t < main_end) ? __ldg(a + j + 8 * t) : 0.0;
+            for (int t = 0; t < T; t++) buf[t] = (j + 8 * t < main_end) ? __ldg(a + j + 8 * t) : 0.0;
         };
-        auto process_group = [&](int l0, const double (&v)[16]) {
+        auto process_group = [&](int l0, const double (&v)[T]) {
             const int leaf = l0 + sub;
             const bool valid = leaf < L;
             const int len = valid ? leaf_len[leaf] : 0;
@@ -356,15 +362,15 @@ __global__ void __launch_bounds__(LB_WARPS * 32, 2) row_stats_kernel(
             const int nvalid = main_end > j ? (main_end - j + 7) >> 3 : 0;  // slots t < nvalid hold data
             double acc = v[0];
 #pragma unroll
-            for (int t = 1; t < 16; t++) acc = __dadd_rn(acc, v[t]);  // pads add +0.0
+            for (int t = 1; t < T; t++) acc = __dadd_rn(acc, v[t]);  // pads add +0.0
             if (do_bracket) {
                 // brackets are whole high-word ranges (host side), so the high
                 // word decides: d = hw - lo_hw, "below" is its sign (all high
                 // words < 2^31) and "inside" is d <= wid
-                npad += 16u - (uint32_t)nvalid;
+                npad += (uint32_t)(T - nvalid);
                 uint32_t nearm = 0;
 #pragma unroll
-                for (int t = 0; t < 16; t++) {
+                for (int t = 0; t < T; t++) {
                     const uint32_t hw = (uint32_t)(dbits(v[t]) >> 32);
                     bool nr = false;
 #pragma unroll
@@ -383,7 +389,7 @@ __global__ void __launch_bounds__(LB_WARPS * 32, 2) row_stats_kernel(
                     if (nearm) {
                         const int t = __ffs(nearm) - 1;
                         nearm &= nearm - 1;
-                        w = pick16(v, t);
+                        w = pick_slot<T>(v, t);
                         const uint32_t hw = (uint32_t)(dbits(w) >> 32);
 #pragma unroll
                         for (int q = 0; q < NB; q++)
@@ -411,12 +417,12 @@ __global__ void __launch_bounds__(LB_WARPS * 32, 2) row_stats_kernel(
             }
             if (j == 0 && valid) lv[leaf] = res;  // leaves l0..l0+3 (lanes 0, 8, 16, 24)
         };
-        double nv[16];
+        double nv[T];
         load_group(0, nv);
         for (int l0 = 0; l0 < L; l0 += 4) {
-            double v[16];
+            double v[T];
 #pragma unroll
-            for (int t = 0; t < 16; t++) v[t] = nv[t];
+            for (int t = 0; t < T; t++) v[t] = nv[t];
             load_group(l0 + 4, nv);
             process_group(l0, v);
         }
@@ -801,9 +807,11 @@ extern "C" int cs_rep_stats_impl(const double* d_resp, int32_t n_groups, int64_t
         cudaMemcpyAsync(b_plan.p, h.data(), sizeof(int32_t) * h.size(), cudaMemcpyHostToDevice, st);
         if ((rc = check_cuda(cudaStreamSynchronize(st), "plan upload"))) return rc;  // h dies here
     }
-    cudaFuncSetAttribute(row_stats_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 16));
-    cudaFuncSetAttribute(row_stats_kernel<MAX_LISTS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)std::max<size_t>(smem, 16));
+    const int max_leaf = pl.leaf_len.empty() ? 0 : *std::max_element(pl.leaf_len.begin(), pl.leaf_len.end());
+    const bool slots12 = max_leaf <= 96;  // 8 lanes x 12 slots cover every leaf's 8-aligned body
+    for (auto k : {row_stats_kernel<3, 12>, row_stats_kernel<3, 16>, row_stats_kernel<MAX_LISTS, 12>,
+                   row_stats_kernel<MAX_LISTS, 16>})
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 16));
     const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((n_rows + LB_WARPS - 1) / LB_WARPS,
                                                                    (int64_t)sm_count() * 8));
     DBuf b_leaf;  // long rows: leaf values in global scratch (one slice per resident warp)
@@ -814,14 +822,11 @@ extern "C" int cs_rep_stats_impl(const double* d_resp, int32_t n_groups, int64_t
     auto leaf_pass = [&](int do_bracket, const int32_t* nl, const uint64_t* lo, const uint64_t* hi,
                          const int64_t* off, const int64_t* cap, unsigned long long* fill,
                          unsigned long long* below, unsigned long long* inside, double* cand) {
-        if (max_brackets <= 3)
-            row_stats_kernel<3><<<blocks, LB_WARPS * 32, std::max<size_t>(smem, 16), st>>>(
-                d_resp, n_rows, rows_per_group, ldr, m, b_plan.as<int32_t>(), L, d_summ, d_row_sums, do_bracket,
-                nl, lo, hi, off, cap, fill, below, inside, cand, n_heights, leaf_scratch);
-        else
-            row_stats_kernel<MAX_LISTS><<<blocks, LB_WARPS * 32, std::max<size_t>(smem, 16), st>>>(
-                d_resp, n_rows, rows_per_group, ldr, m, b_plan.as<int32_t>(), L, d_summ, d_row_sums, do_bracket,
-                nl, lo, hi, off, cap, fill, below, inside, cand, n_heights, leaf_scratch);
+        auto k = max_brackets <= 3 ? (slots12 ? row_stats_kernel<3, 12> : row_stats_kernel<3, 16>)
+                                   : (slots12 ? row_stats_kernel<MAX_LISTS, 12> : row_stats_kernel<MAX_LISTS, 16>);
+        k<<<blocks, LB_WARPS * 32, std::max<size_t>(smem, 16), st>>>(
+            d_resp, n_rows, rows_per_group, ldr, m, b_plan.as<int32_t>(), L, d_summ, d_row_sums, do_bracket,
+            nl, lo, hi, off, cap, fill, below, inside, cand, n_heights, leaf_scratch);
         return check_launch("row_stats_kernel");
     };
     auto combine = [&]() { return CS_OK; };  // the tree is combined on chip
