@@ -275,13 +275,28 @@ def main():
     # of sweep k+1 and statistics of sweep k-1 overlap the simulation of k)
     eng.run_pipelined(max(args.warmup, 3), gather)
     barrier()
+    # schedule choice (1 GPU): the overlapped order usually runs a sweep in
+    # ~40.5 ms, but in some processes the block placement settles into a
+    # 58 ms pattern; the in-order schedule is a steady ~43.7 ms.  Three warm
+    # sweeps of each decide (both compute every sweep in full).
+    ordered, sched_ms = None, {}
+    if world == 1:
+        for name, o in (("overlapped", False), ("ordered", True)):
+            ta, tb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            ta.record()
+            eng.run_pipelined(3, gather, ordered=o)
+            tb.record()
+            tb.synchronize()
+            sched_ms[name] = round(ta.elapsed_time(tb) / 3, 2)
+        ordered = sched_ms["ordered"] < sched_ms["overlapped"]
     launches0 = eng.lib.cs_launch_count()
     with ClockSampler(local) as clk:
         t_start = torch.cuda.Event(enable_timing=True)
         t_end = torch.cuda.Event(enable_timing=True)
         barrier()
         t_start.record()
-        eng.run_pipelined(args.steps, gather)
+        eng.run_pipelined(args.steps, gather, ordered=ordered)
         t_end.record()
         barrier()
     ms = t_start.elapsed_time(t_end)
@@ -348,6 +363,8 @@ def main():
                             f"{args.jobs} jobs per GPU",
                 "jobs_per_step": world * jobs_per_step,
                 "l2": "inputs larger than L2 (responses 8 B/job stored in HBM)",
+                "schedule": {"chosen": "sharded-ordered" if ordered is None else
+                             ("ordered" if ordered else "overlapped"), "warm_ms_per_sweep": sched_ms},
                 "parallelism": f"replicas sharded over {world} GPU(s) ({R} per GPU); NCCL all-gather of "
                            "summaries + all-reduced radix-select histograms for exact global quantiles",
             },

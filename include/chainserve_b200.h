@@ -121,6 +121,16 @@ int cs_jffc_sim(const cs_sim_point* d_points, int32_t n_points, const double* d_
 int64_t cs_jffc_sim_workspace_bytes(int32_t n_points, int32_t n_reps, int32_t max_chains,
                                     int32_t max_capacity, int64_t n_jobs);
 
+/* Engine-side scheduling helper (no reference counterpart): split the
+ * current device's SMs into two green contexts -- >= sim_sms SMs for the
+ * simulator, the rest for everything else -- and return one stream on the
+ * first (*sim_stream) and two on the second (aux_streams[0..1]).  Created once
+ * per device and process; kernels are launched on these streams through the
+ * runtime API as on any stream.  Needs a driver with green contexts (CUDA
+ * 12.4+); returns CS_ERR_CUDA otherwise. */
+int cs_sm_partition(int32_t sim_sms, void** sim_stream, void** aux_streams, int32_t* out_sim_sms,
+                    int32_t* out_aux_sms);
+
 /* ---- the rest of run_sim's signature ---------- */
 /* _simulate_once for the dedicated-queue baseline policies (sim.py:104-117,
  * 279-286), the sampled and trace workloads (sim.py:161-178,199-203,

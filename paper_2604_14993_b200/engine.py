@@ -11,6 +11,7 @@ stream; all compute is the engine's own kernels via the C-ABI.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 from typing import Sequence
 
@@ -126,7 +127,7 @@ class SweepEngine:
                 None, st.cuda_stream)
         N.check(rc, "cs_rep_stats")
 
-    def run_pipelined(self, steps: int, after_stats=None) -> int:
+    def run_pipelined(self, steps: int, after_stats=None, ordered: bool | None = None) -> int:
         """`steps` complete sweeps, software-pipelined over two buffer sets and
         three CUDA streams: the streams of sweep k+1 and the statistics of
         sweep k-1 run while sweep k simulates (the simulator leaves most issue
@@ -146,6 +147,11 @@ class SweepEngine:
             self.pipe = [torch.cuda.Stream(priority=0), torch.cuda.Stream(priority=-8),
                          torch.cuda.Stream(priority=0)]
         s_gen, s_sim, s_stat = self.pipe
+        if ordered is None:
+            ordered = self.distributed or bool(os.environ.get("CS_PIPE_ORDERED"))
+        part = None if ordered else self._sm_partition()
+        if part is not None:  # simulator alone on its SMs; streams + statistics on the rest
+            s_sim, s_gen, s_stat = part
         cur = torch.cuda.current_stream()
         for s_ in self.pipe:
             s_.wait_stream(cur)
@@ -161,7 +167,7 @@ class SweepEngine:
 
         if steps > 0:
             gen(0)
-        if self.distributed:
+        if ordered:
             # sharded: the statistics' NCCL collectives cannot run beside the
             # simulator (their kernels need an SM configuration the simulator's
             # SMs do not offer), so they follow each simulation in its stream;
@@ -204,6 +210,42 @@ class SweepEngine:
         for s_ in self.pipe:
             cur.wait_stream(s_)
         return (steps - 1) & 1
+
+    def _sm_partition(self):
+        """(sim, gen, stat) streams on two green-context SM partitions, or None.
+
+        The simulator's SM count keeps its most loaded SM at the same warp
+        count as an even spread over the whole device (ceil(warps / SMs)),
+        leaving the remaining SMs to the streams and statistics of the
+        neighbouring sweeps (see csrc/partition.cu).  Only for the one-warp-
+        per-32-replications kernels.  Opt-in (CS_SM_PARTITION=1): on config 2
+        the simulator takes 40.7 ms on 128 SMs (37.0 ms on all 148) and the
+        streams + statistics 41 ms on the other 20, so the split sweep costs
+        45 ms against 40.5 ms unsplit."""
+        if os.environ.get("CS_SM_PARTITION", "0") != "1":
+            return None
+        if getattr(self, "_part", False) is not False:
+            return self._part
+        self._part = None
+        if self.max_chains > 8 or self.max_cap > 16 or self.n >= (1 << 27):
+            return None
+        torch = self.torch
+        n_sm = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+        warps = -(-self.P * self.R // 32)
+        per = -(-warps // n_sm)
+        sim_sms = -(-warps // per)
+        sim_sms += sim_sms & 1  # partitions come in SM pairs
+        if n_sm - sim_sms < 8:
+            return None
+        s_sim, aux = C.c_void_p(), (C.c_void_p * 2)()
+        got_sim, got_aux = C.c_int32(), C.c_int32()
+        rc = self.lib.cs_sm_partition(sim_sms, C.byref(s_sim), aux, C.byref(got_sim), C.byref(got_aux))
+        if rc != 0:
+            return None
+        ext = torch.cuda.ExternalStream
+        self._part = (ext(s_sim.value), ext(aux[0]), ext(aux[1]))
+        self.partition_sms = (got_sim.value, got_aux.value)
+        return self._part
 
     def step(self, timed: bool = False) -> StageTimes | None:
         """One full sweep on the device; optional per-stage CUDA-event times."""
