@@ -285,12 +285,16 @@ def test_sample_select_and_fused_pairwise_means(eng, oracle):
         assert np.array_equal(bits(res.summaries[p]["resp_mean"]), bits(means))
 
 
-def test_sweep_engine_pipelined_equals_unpipelined(eng):
+@pytest.mark.parametrize("schedule", ["overlapped", "ordered", "sm_partition"])
+def test_sweep_engine_pipelined_equals_unpipelined(eng, schedule, monkeypatch):
     """SweepEngine.run_pipelined (two buffer sets, three CUDA streams; the
-    benchmark's timed loop) computes every sweep exactly like step()."""
+    benchmark's timed loop) computes every sweep exactly like step(), in
+    either order and on green-context SM partitions."""
     import torch
 
     from paper_2604_14993_b200.engine import SweepEngine
+
+    monkeypatch.setenv("CS_SM_PARTITION", "1" if schedule == "sm_partition" else "0")
 
     service, servers, _ = eng.petals_instance(10, 0.2, 101)
     system = eng.greedy_cache_allocation(
@@ -300,8 +304,10 @@ def test_sweep_engine_pipelined_equals_unpipelined(eng):
     e.step()
     torch.cuda.synchronize()
     ref_s, ref_b, ref_o = e.summaries(0).copy(), e.busy(0).copy(), e.order_stats()
-    last = e.run_pipelined(3)
+    last = e.run_pipelined(3, ordered=schedule == "ordered")
     torch.cuda.synchronize()
+    if schedule == "sm_partition":
+        assert getattr(e, "partition_sms", (0, 0))[1] > 0  # the partition was made and used
     for b in (0, 1):  # both buffer sets hold a complete, identical sweep
         assert np.array_equal(e.summaries(b).view(np.uint8), ref_s.view(np.uint8)), b
         assert np.array_equal(bits(e.busy(b)), bits(ref_b)), b
