@@ -829,7 +829,6 @@ extern "C" int cs_rep_stats_impl(const double* d_resp, int32_t n_groups, int64_t
             nl, lo, hi, off, cap, fill, below, inside, cand, n_heights, leaf_scratch);
         return check_launch("row_stats_kernel");
     };
-    auto combine = [&]() { return CS_OK; };  // the tree is combined on chip
     const RowView full{m, 40, 40};  // contiguous
     // one 32-byte sector (4 responses) of every 128: 1/32 of the bytes, and far
     // less autocorrelated (queueing makes consecutive responses similar) than
@@ -837,8 +836,7 @@ extern "C" int cs_rep_stats_impl(const double* d_resp, int32_t n_groups, int64_t
     const int64_t n_chunks = m / 128, tail = std::min<int64_t>(4, m % 128);
     const RowView sample{n_chunks * 4 + tail, 2, 7};
     if (!want_ranks || N <= (1 << 20) || sample.len < 64) {
-        if ((rc = leaf_pass(0, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr)) ||
-            (rc = combine()))
+        if ((rc = leaf_pass(0, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr)))
             return rc;
         if (!want_ranks) return CS_OK;
         std::vector<double> vals;  // small groups: exact selection over all values
@@ -849,7 +847,6 @@ extern "C" int cs_rep_stats_impl(const double* d_resp, int32_t n_groups, int64_t
     }
     const int64_t NS = rows_per_group * sample.len * shards;  // sample size per group
     const size_t T = target.size();
-    bool combined = false;
     double widen = 1.0;
     for (int attempt = 0; attempt < 4; attempt++, widen *= 8.0) {
         // ---- 1. sample order statistics bracketing each target ----
@@ -946,10 +943,6 @@ extern "C" int cs_rep_stats_impl(const double* d_resp, int32_t n_groups, int64_t
                             b_cap.as<int64_t>(), b_fill.as<unsigned long long>(), b_below.as<unsigned long long>(), b_inside.as<unsigned long long>(),
                             b_cand.as<double>())))
             return rc;
-        if (!combined) {
-            if ((rc = combine())) return rc;
-            combined = true;
-        }
         // fill = reserved slots (the candidate lists' lengths, sealed tails
         // included); inside = values actually inside the brackets
         std::vector<unsigned long long> fill(L6), below(L6), inside_all(L6), overflow(L6);
