@@ -18,8 +18,10 @@
 //      select on the IEEE bit patterns (responses >= +0, so bit order ==
 //      value order): 15-bit digit-0 histogram, compaction of the selected
 //      buckets, 12-bit digit rounds.
-//   2. the leaf-sum pass also counts the values below each bracket and
-//      compacts the values inside it (warp-aggregated appends).
+//   2. the leaf-sum pass also counts the values below each bracket (whole
+//      high-word ranges: the high 32 bits decide) and compacts the values
+//      inside it (per-warp chunk reservations, no returning atomic on the
+//      append path; unused reserved slots sort above every response).
 //   3. if below <= k < below + |inside| (verified; else the bracket widens and
 //      step 2 repeats), the k-th value is found by 12-bit digit rounds over
 //      the few candidates, starting below the bracket's common bit prefix.
@@ -105,24 +107,6 @@ __global__ void __launch_bounds__(1024) hist0_rows_kernel(const double* __restri
         for (int b = threadIdx.x; b < H0_BINS; b += blockDim.x)
             if (sh[b]) atomicAdd(&gh[b], sh[b]);
         __syncthreads();
-    }
-}
-
-// Warp-aggregated append of v to candidate list `list` (every lane calls it).
-__device__ __forceinline__ void append(int list, double v, unsigned long long* __restrict__ fill,
-                                       const int64_t* __restrict__ off, const int64_t* __restrict__ cap,
-                                       double* __restrict__ cand) {
-    const int lane = threadIdx.x & 31;
-    const unsigned active = __ballot_sync(0xffffffffu, list >= 0);
-    if (list >= 0) {
-        const unsigned peers = __match_any_sync(active, list);
-        const int leader = __ffs(peers) - 1;
-        const int rank_in = __popc(peers & ((1u << lane) - 1));
-        unsigned long long base = 0;
-        if (lane == leader) base = atomicAdd(&fill[list], (unsigned long long)__popc(peers));
-        base = __shfl_sync(peers, base, leader);
-        const int64_t pos = (int64_t)base + rank_in;
-        if (pos < cap[list]) cand[off[list] + pos] = v;  // overflow is detected by the host
     }
 }
 
