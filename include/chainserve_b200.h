@@ -104,12 +104,20 @@ typedef struct {
  * row (the simulator's cursors and prefetches run ahead without clamping).
  * Outputs are point-major, o = p*n_reps_total + rep_begin + r:
  *   d_responses[o*ldr + q]  q < n-warm, completion order (NULL: not stored;
- *                           ldr must be even -- rows are written with 16-byte stores)
+ *                           ldr even: the single-chain path writes whole
+ *                           lines with 16-byte stores; a multiple of 16
+ *                           keeps every line 128-byte aligned)
  *   d_busy[o*ldb + k]       busy_time_s (ldb >= max_chains)
  *   d_summary[o]
  *   d_jobs[(o*n + j)*4 ..]  (arrival, start, finish, chain) or NULL.
- * max_chains / max_capacity bound K and sum(caps) over the points; above 8 /
- * 16 a generic kernel needs cs_jffc_sim_workspace_bytes() of d_workspace.
+ * Single-chain compositions (K = 1, C <= 16) without d_jobs take the
+ * segmented time-parallel kernel (csrc/jffc_seg.cu): responses, counted,
+ * window, lambda_effective and end_queue bit-exact; wait/service sums,
+ * occupancy areas and busy time summed per job in fixed job blocks
+ * (reassociated, ~1e-13 relative).  Environment CS_SIM_EXACT=1 selects the
+ * serial kernel that is bit-exact in every field.  That path and the
+ * generic kernel (K > 512 or C > 1024) need cs_jffc_sim_workspace_bytes()
+ * of d_workspace.
  * warm = int(warmup_fraction * n) computed by the caller as Python does. */
 int cs_jffc_sim(const cs_sim_point* d_points, int32_t n_points, const double* d_rates,
                 const int32_t* d_caps, int32_t max_chains, int32_t max_capacity,
@@ -121,15 +129,11 @@ int cs_jffc_sim(const cs_sim_point* d_points, int32_t n_points, const double* d_
 int64_t cs_jffc_sim_workspace_bytes(int32_t n_points, int32_t n_reps, int32_t max_chains,
                                     int32_t max_capacity, int64_t n_jobs);
 
-/* Engine-side scheduling helper (no reference counterpart): split the
- * current device's SMs into two green contexts -- >= sim_sms SMs for the
- * simulator, the rest for everything else -- and return one stream on the
- * first (*sim_stream) and two on the second (aux_streams[0..1]).  Created once
- * per device and process; kernels are launched on these streams through the
- * runtime API as on any stream.  Needs a driver with green contexts (CUDA
- * 12.4+); returns CS_ERR_CUDA otherwise. */
-int cs_sm_partition(int32_t sim_sms, void** sim_stream, void** aux_streams, int32_t* out_sim_sms,
-                    int32_t* out_aux_sms);
+/* Engine-side introspection (no reference counterpart): the launch plan of
+ * the segmented single-chain path for this shape on the current device --
+ * out[0] segments per replication, out[1] warps per segment, out[2]
+ * checkpoints per segment, out[3] the slot-count instance (4/7/8/16). */
+int cs_seg_plan(int32_t n_points, int32_t n_reps, int32_t max_capacity, int64_t n_jobs, int32_t* out);
 
 /* ---- the rest of run_sim's signature ---------- */
 /* _simulate_once for the dedicated-queue baseline policies (sim.py:104-117,

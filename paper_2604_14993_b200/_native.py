@@ -65,7 +65,7 @@ assert SUMMARY_DTYPE.itemsize == C.sizeof(RepSummary)
 
 EXPORTS = (
     "cs_version", "cs_last_error", "cs_host_log1p_variant", "cs_device_count", "cs_launch_count",
-    "cs_philox_keys", "cs_exp_streams", "cs_jffc_sim", "cs_jffc_sim_workspace_bytes", "cs_sm_partition",
+    "cs_philox_keys", "cs_exp_streams", "cs_jffc_sim", "cs_jffc_sim_workspace_bytes", "cs_seg_plan",
     "cs_rep_stats", "cs_rep_stats_dist", "cs_run_sim_host", "cs_gbp_batch", "cs_gca_batch",
     "cs_nccl_unique_id", "cs_comm_init", "cs_comm_destroy", "cs_occupancy_bounds",
     "cs_birth_death_occupancy", "cs_sim_ext", "cs_ragged_rows",
@@ -98,8 +98,7 @@ def load(require_device: bool = True):
         L.cs_jffc_sim_workspace_bytes.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                                   C.c_int64]
         L.cs_jffc_sim_workspace_bytes.restype = C.c_int64
-        L.cs_sm_partition.argtypes = [C.c_int32, P(C.c_void_p), P(C.c_void_p), P(C.c_int32), P(C.c_int32)]
-        L.cs_sm_partition.restype = C.c_int
+        L.cs_seg_plan.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_int64, P(C.c_int32)]
         L.cs_rep_stats.argtypes = [vp, C.c_int32, C.c_int64, C.c_int64, C.c_int64, vp,
                                    P(C.c_int64), C.c_int32, P(C.c_double), vp, vp]
         L.cs_rep_stats_dist.argtypes = L.cs_rep_stats.argtypes
@@ -159,3 +158,10 @@ def seed_words(seed: int) -> np.ndarray:
         words.append(seed & 0xFFFFFFFF)
         seed >>= 32
     return np.asarray(words, dtype=np.uint32)
+
+
+def seg_plan(n_points: int, n_reps: int, max_capacity: int, n_jobs: int) -> dict:
+    """Launch plan of the segmented single-chain simulator for this shape."""
+    out = (C.c_int32 * 4)()
+    check(load().cs_seg_plan(n_points, n_reps, max_capacity, n_jobs, out), "cs_seg_plan")
+    return {"segments": out[0], "warps_per_segment": out[1], "checkpoints": out[2], "cmax": out[3]}

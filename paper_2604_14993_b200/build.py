@@ -21,7 +21,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 BUILD = os.path.join(ROOT, "build", "csrc")
 LIB = os.path.join(PKG, "libchainserve_b200.so")
-SOURCES = ["capi.cu", "exp_stream.cu", "jffc_sim.cu", "stats.cu", "compose.cu", "dist.cu", "bounds.cu", "sim_ext.cu", "partition.cu"]
+SOURCES = ["capi.cu", "exp_stream.cu", "jffc_sim.cu", "jffc_seg.cu", "stats.cu", "compose.cu", "dist.cu", "bounds.cu", "sim_ext.cu"]
 
 
 def nccl_dirs():

@@ -267,6 +267,11 @@ int cs_run_sim_host(const cs_sim_point* points, int32_t n_points, const double* 
         set_error("cs_run_sim_host: no CUDA device");
         return CS_ERR_CUDA;
     }
+    if (n_jobs < 1 || warm < 0 || warm >= n_jobs || n_reps < 0 || n_points < 0 || rep_begin < 0) {
+        set_error("cs_run_sim_host: invalid sizes (need n_jobs >= 1, 0 <= warm < n_jobs)");
+        return CS_INVALID;
+    }
+    if (n_reps == 0 || n_points == 0) return CS_OK;
     cudaStream_t st = (cudaStream_t)stream;
     ensure_mem_pool();
     int rc = CS_OK;
@@ -282,7 +287,7 @@ int cs_run_sim_host(const cs_sim_point* points, int32_t n_points, const double* 
         return CS_INVALID;
     }
     const int64_t m = n_jobs - warm;
-    const int64_t ldr = (m + 1) & ~1ll;
+    const int64_t ldr = (m + 15) & ~15ll;  // rows start on 128-byte lines
     const int64_t lds = 2 * n_jobs;
     const int64_t rows = (int64_t)n_points * n_reps;
     // replications per stream chunk (bounded stream scratch)

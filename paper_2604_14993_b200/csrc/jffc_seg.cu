@@ -1,0 +1,886 @@
+// jffc_seg.cu -- time-parallel single-chain JFFC simulation (K = 1, C <= 16).
+//
+// The reference's replication (sim.py:255-296) is one serial event loop.
+// With one chain of capacity C it is FCFS over C identical slots: job j
+// starts at st_j = max(a_j, W[0]) where W is the sorted multiset of slot
+// free times (Kiefer-Wolfowitz; the per-JOB recursion of jffc_sim.cu's k1
+// kernel).  This file splits every replication into S job-index SEGMENTS
+// [b_s, b_{s+1}) simulated concurrently (one thread per (segment, row)):
+//
+//  * segment s starts from an EMPTY system at job b_s (its arrival time
+//    a_{b_s} comes from an exact sequential cumsum pre-pass, the very
+//    operations np.cumsum performs).  Its W is a lower bound of the true W.
+//  * the true trajectory and segment s's run COUPLE at the first step j
+//    where the two W's are identical (finish times, job identities and the
+//    emission count): from there on every start, finish and emission is the
+//    same IEEE operation on the same operands, so segment s's results are
+//    bit-exact from j on.  Segment 0 is exact from job 0.
+//  * an exact segment runs past its range end ("phase 2") and compares its
+//    W with the next segment's checkpoints (stored during that segment's own
+//    run); on a match it hands over and stops.  If it passes a whole segment
+//    without coupling, that segment is marked SKIPPED and the exact one keeps
+//    going (worst case: one serial replication, e.g. for rho >= 1).
+//  * responses are written in completion order at the position the exact
+//    run would give them: a segment's emission counter starts at the number
+//    of counted jobs before b_s, which equals the exact count at the coupling
+//    step (both W's hold the same jobs).  Garbage written by a segment before
+//    it was coupled into is overwritten by the exact predecessor's phase 2,
+//    which first waits until that segment's phase 1 is DONE.
+//  * per-job sums: wait/service (sim.py:238-240) and the time integrals of
+//    the number in system and in service over the windows (area, busy,
+//    sim.py:224-231) are accumulated PER JOB as clipped intervals
+//    [max(a, w_start), min(f, T)) instead of per event; the owner chain of
+//    segments is summed by the finalize kernel.  These sums are therefore
+//    reassociated (agree to ~1e-13 relative, asserted <= 1e-12 in the tests);
+//    responses, their order, counted, window, lambda_eff and end_queue are
+//    bit-exact.  CS_SIM_EXACT=1 selects jffc_sim.cu's serial kernel, which
+//    replays the reference's event order and is bit-exact in every field.
+//
+// All segments of a launch must be resident at once (phase-2 waits): the
+// kernel is launched cooperatively and S is chosen from the occupancy.
+//
+// Responses are staged per lane in a shared-memory ring and flushed as whole
+// 128-byte lines, 8 threads per line with 16-byte stores (4 lines per warp
+// store instruction) instead of one scattered 8-byte store per lane per job.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdlib.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <vector>
+
+#include "cs_internal.cuh"
+
+namespace cs {
+namespace seg {
+
+constexpr int NAGG = 6;  // wait, service, area_mid, area_end, busy, end_queue
+constexpr int AG_WAIT = 0, AG_SERV = 1, AG_AMID = 2, AG_AEND = 3, AG_BUSY = 4, AG_ENDQ = 5;
+// job blocks: every per-job sum is accumulated per global block of BS jobs
+// (sequentially inside the block) and the blocks are added in order by the
+// finalize kernel -- one fixed association for a given n, whatever the
+// segment count, the batch shape or the GPU count
+constexpr int64_t BS = 256;
+constexpr int MAXQ = 20;
+constexpr uint32_t DONE = 1u << 30;
+constexpr int32_t ST_UNKNOWN = 0, ST_SKIPPED = 1;  // status >= 2: EXACT, coupled at job (status - 2)
+
+// checkpoint offsets from a segment's first job, in blocks: dense first
+// (typical coupling within 32-300 jobs), sparser for the rho -> 1 tails
+__host__ __device__ inline int64_t ck_offset(int q) {
+    // 1..8, 10..16 step 2, 20..32 step 4, 40..64 step 8 blocks
+    const int m = q <= 8 ? q : q <= 12 ? 2 * q - 8 : q <= 16 ? 4 * q - 32 : 8 * q - 96;
+    return BS * m;
+}
+
+__host__ __device__ inline int64_t seg_begin(int s, int S, int64_t n) {
+    if (s <= 0) return 0;
+    if (s >= S) return n;
+    return ((int64_t)s * n / S) / BS * BS;
+}
+
+struct Args {
+    const cs_sim_point* pts;
+    const double* rates;
+    const int32_t* caps;
+    const double* S;  // streams [R][lds]
+    int64_t lds;
+    int32_t P, R, RT, rb;
+    int64_t n, warm;
+    double* resp;
+    int64_t ldr;
+    double* busy_out;
+    int32_t ldb;
+    cs_rep_summary* summ;
+    // workspace
+    double* prefix;    // [T][S + 3]: a_{b_s} (s < S), w_start, t_mid, t_end
+    double* ckf;       // [S][G][Q][CMAX + 1][32]   fin[CMAX], n_resp (bits)
+    uint32_t* ckk;     // [S][G][Q][CMAX][32]       keys
+    double* blk;       // [NB][NAGG][T]             per-block sums
+    int32_t* status;   // [S][T]
+    uint32_t* progress;  // [S][G]
+    int32_t nseg, G, Q, cmax;
+    int64_t nblk;
+    unsigned long long* trace;  // development: [blocks][4] globaltimer stamps or NULL
+};
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ int32_t ld_acquire(const int32_t* p) {
+    int32_t v;
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(int32_t* p, int32_t v) {
+    asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void prefetch_l1_if(const void* a, bool c) {
+    asm volatile("{.reg .pred p; setp.ne.u32 p, %1, 0; @p prefetch.global.L1 [%0];}" ::"l"(a), "r"((unsigned)c));
+}
+__device__ __forceinline__ void prefetch_l2_if(const void* a, bool c) {
+    asm volatile("{.reg .pred p; setp.ne.u32 p, %1, 0; @p prefetch.global.L2 [%0];}" ::"l"(a), "r"((unsigned)c));
+}
+__device__ __forceinline__ void st_v2(double* p, double x, double y) {
+    asm volatile("st.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(x), "d"(y) : "memory");
+}
+__device__ __forceinline__ double dmax0(double x) { return x > 0.0 ? x : 0.0; }
+
+// ---------------------------------------------------------------------------
+// Pre-pass: the exact arrival times at the segment starts and at the
+// warm-up / mid / last arrivals (np.cumsum order: a_0 = x_0, a_i = a_{i-1} + x_i,
+// x_i = (1/lam) * S_i, sim.py:147).  One thread per row, lanes of a warp share
+// streams (the P points of a rep), so the stream loads are broadcasts.
+// ---------------------------------------------------------------------------
+constexpr int PF_U = 16;     // values per chunk (one 128-byte line of a row)
+constexpr int PF_NBUF = 12;  // chunks in flight (cp.async ring)
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+__global__ void __launch_bounds__(32) seg_prefix_kernel(Args A) {
+    // the warp's distinct stream rows (lanes of a rep share one): chunk k
+    // of local row q at ring[k % NBUF][q][0..16)
+    extern __shared__ __align__(16) double pf_ring[];
+    const int lane = threadIdx.x;
+    const int64_t T = (int64_t)A.P * A.R;
+    const int64_t tid0 = (int64_t)blockIdx.x * 32 + lane;
+    const bool valid = tid0 < T;
+    const int64_t tid = valid ? tid0 : (int64_t)blockIdx.x * 32;
+    const int32_t r = (int32_t)(tid / A.P), p = (int32_t)(tid % A.P);
+    const int32_t r_lo = (int32_t)(((int64_t)blockIdx.x * 32) / A.P);
+    const int64_t t_last = min((int64_t)blockIdx.x * 32 + 31, T - 1);
+    const int nr = (int)(t_last / A.P) - r_lo + 1;  // distinct rows, <= 32
+    const int q_own = r - r_lo;
+    const double scale = __ddiv_rn(1.0, A.pts[p].lam);
+    const int32_t n = (int32_t)A.n, warm = (int32_t)A.warm, mid = warm + (n - warm) / 2;
+    const int S = A.nseg;
+    double* out = A.prefix + tid * (S + 3);
+    // recorded job indices (uniform over the grid): segment starts, warm-up,
+    // mid and last arrival
+    int si = 1;
+    bool got_w = false, got_m = false;
+    auto next_ev = [&]() {  // smallest index not recorded yet
+        int32_t ev = n - 1;
+        if (si < S) ev = min(ev, (int32_t)seg_begin(si, S, n));
+        if (!got_w) ev = min(ev, warm);
+        if (!got_m) ev = min(ev, mid);
+        return ev;
+    };
+    auto record = [&](int32_t j, double a) {
+        while (si < S && seg_begin(si, S, n) == j) {
+            if (valid) out[si] = a;
+            si++;
+        }
+        if (!got_w && j == warm) {
+            if (valid) out[S] = a;
+            got_w = true;
+        }
+        if (!got_m && j == mid) {
+            if (valid) out[S + 1] = a;
+            got_m = true;
+        }
+        if (j == n - 1 && valid) out[S + 2] = a;
+    };
+    // one sequential cumsum (the DADD chain is the critical path); stream
+    // lines staged NBUF-1 chunks ahead through cp.async, 8 lanes per line
+    const int nchunks = (n + PF_U - 1) / PF_U;
+    const int piece = lane & 7;
+    auto issue = [&](int k) {
+        if (k < nchunks) {
+            for (int q0 = 0; q0 < nr; q0 += 4) {
+                const int q = q0 + (lane >> 3);
+                if (q < nr) {
+                    const double* src = A.S + (int64_t)(r_lo + q) * A.lds + (int64_t)k * PF_U + 2 * piece;
+                    cp_async16(pf_ring + ((size_t)(k % PF_NBUF) * nr + q) * PF_U + 2 * piece, src);
+                }
+            }
+        }
+        cp_async_commit();
+    };
+    for (int k = 0; k < PF_NBUF - 1; k++) issue(k);
+    // x[] holds chunk k already scaled (the DMULs and shared loads of chunk
+    // k+1 overlap the DADD chain of chunk k)
+    double x[PF_U];
+    cp_async_wait<PF_NBUF - 2>();
+    __syncwarp();
+#pragma unroll
+    for (int u = 0; u < PF_U; u++) x[u] = __dmul_rn(scale, pf_ring[(size_t)q_own * PF_U + u]);
+    double a = x[0];
+    if (valid) out[0] = a;
+    int32_t ev = next_ev();
+    for (int k = 0; k < nchunks; k++) {
+        __syncwarp();  // every lane is done with the slot chunk k-1 used
+        issue(k + PF_NBUF - 1);
+        cp_async_wait<PF_NBUF - 2>();  // chunk k+1 landed
+        __syncwarp();
+        double y[PF_U];
+        const double* c = pf_ring + ((size_t)((k + 1) % PF_NBUF) * nr + q_own) * PF_U;
+#pragma unroll
+        for (int u = 0; u < PF_U; u++) y[u] = c[u];
+        const int32_t j0 = k * PF_U;
+        if (j0 > 0 && ev >= j0 + PF_U) {  // no recorded index in this chunk: plain cumsum
+#pragma unroll
+            for (int u = 0; u < PF_U; u++) a = __dadd_rn(a, x[u]);
+        } else {
+#pragma unroll
+            for (int u = 0; u < PF_U; u++) {
+                const int32_t j = j0 + u;
+                if (j > 0) a = __dadd_rn(a, x[u]);
+                if (j == ev) {
+                    record(j, a);
+                    ev = j == n - 1 ? INT32_MAX : next_ev();
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < PF_U; u++) x[u] = __dmul_rn(scale, y[u]);
+    }
+    cp_async_wait<0>();
+}
+
+// ---------------------------------------------------------------------------
+// The segment kernel.  Block = one warp = 32 rows (lanes) of one segment.
+// ---------------------------------------------------------------------------
+enum { PH_A = 0, PH_B = 1, PH_C = 2 };  // before warm-up / first / second half of the window
+
+template <int CMAX>
+__global__ void __launch_bounds__(32) jffc_seg_kernel(Args A) {
+    constexpr int ID_BITS = CMAX <= 8 ? 3 : 4;
+    constexpr uint32_t DUMMY = 0x80000000u;  // an initially idle slot, not a job
+    constexpr uint32_t J_MASK = (1u << (31 - ID_BITS)) - 1;
+    constexpr uint32_t ID_MASK = (1u << ID_BITS) - 1;
+    constexpr int FCK = CMAX + 1;
+    constexpr unsigned FULL = 0xffffffffu;
+
+    // response ring: element (pos, lane) at [(pos >> 1) & 15][lane][pos & 1], row pitch 66 doubles
+    __shared__ __align__(16) double sh_ring[16 * 66];
+    __shared__ double sh_rbuf[CMAX * 32];  // response of the job holding slot id
+    __shared__ double* sh_row[32];         // response row of each lane
+    __shared__ int4 sh_meta[32];           // per-lane flush line: start, first, end, has
+
+    const int lane = threadIdx.x;
+    const int S = A.nseg, G = A.G, Q = A.Q;
+    const int s = blockIdx.x / G, g = blockIdx.x % G;
+    const int64_t T = (int64_t)A.P * A.R;
+    const int64_t tid = (int64_t)g * 32 + lane;
+    const bool valid = tid < T;
+    const int64_t te = valid ? tid : 0;
+    const int32_t r = (int32_t)(te / A.P), p = (int32_t)(te % A.P);
+    const int64_t o = (int64_t)p * A.RT + A.rb + r;
+    const int64_t n = A.n, warm = A.warm, mid = warm + (n - warm) / 2;
+    const cs_sim_point pt = A.pts[p];
+    const double inv_mu = __ddiv_rn(1.0, A.rates[pt.chain_base]);
+    const int32_t cap = A.caps[pt.chain_base];
+    const double scale = __ddiv_rn(1.0, pt.lam);
+    const double* __restrict__ gap = A.S + (int64_t)r * A.lds;
+    const double* __restrict__ szs = gap + n;
+    const double* pre = A.prefix + te * (S + 3);
+    const double Ws = pre[S], Tm = pre[S + 1], Te = pre[S + 2];
+    sh_row[lane] = (A.resp && valid) ? A.resp + o * A.ldr : nullptr;
+    const bool writes = A.resp != nullptr;
+    double* blk = A.blk + te;
+
+    const int64_t b = seg_begin(s, S, n), e = seg_begin(s + 1, S, n);
+    const int unit = s * G + g;
+    unsigned long long* tr = A.trace ? A.trace + (int64_t)blockIdx.x * 4 : nullptr;
+    if (tr && lane == 0) tr[0] = gtimer();
+
+    // ---- lane state
+    double fin[CMAX];
+    uint32_t key[CMAX];
+#pragma unroll
+    for (int k = 0; k < CMAX; k++) {
+        fin[k] = k < cap ? -INFINITY : INFINITY;
+        key[k] = DUMMY | (uint32_t)k;
+    }
+    double* rbuf = sh_rbuf + lane;
+    // positions are < n - warm < 2^27: 32-bit
+    int32_t n_resp = (int32_t)(b > warm ? b - warm : 0);  // counted jobs before b = the exact position at coupling
+    int32_t fl_lo = n_resp;                               // first position not yet flushed
+    double ag[NAGG];
+#pragma unroll
+    for (int k = 0; k < NAGG; k++) ag[k] = 0.0;
+    bool act = valid;  // lane simulates / writes / accumulates
+
+    int32_t j = (int32_t)b;
+    const int32_t warm32 = (int32_t)warm;
+    double a = pre[s];  // a_b
+    const double* __restrict__ gp = gap + b + 1;  // gap of job j+1
+    const double* __restrict__ sp = szs + b;      // size of job j
+    double g1 = __ldg(gp), g2 = __ldg(gp + 1), sz = __ldg(sp), sz1 = __ldg(sp + 1);
+    __syncwarp();
+
+    // ---- helpers (warp-uniform control flow) ---------------------------
+    auto ring_put = [&](int32_t pos, double v) {
+        sh_ring[((pos >> 1) & 15) * 66 + 2 * lane + (pos & 1)] = v;
+    };
+    // flush complete lines (final: also the trailing partial line) of the
+    // lanes in `who`; lines go out 4 per warp instruction, 8 threads x 16 B
+    // each; the first and last line of a lane's range element by element.
+    auto flush = [&](bool final, bool who) {
+        for (;;) {
+            const int32_t ls = fl_lo & ~15;
+            const int32_t hi_full = ls + 16;
+            const bool has = who && (final ? fl_lo < n_resp : hi_full <= n_resp);
+            const int32_t hi = hi_full < n_resp ? hi_full : n_resp;
+            const unsigned mask = __ballot_sync(FULL, has);
+            if (!mask) break;
+            if (writes) {
+                sh_meta[lane] = make_int4(ls, fl_lo, hi, has ? 1 : 0);
+                __syncwarp();
+                const int grp = lane >> 3, c = lane & 7;
+#pragma unroll 1
+                for (int L0 = 0; L0 < 32; L0 += 4) {
+                    if (((mask >> L0) & 15u) == 0) continue;
+                    const int L = L0 + grp;
+                    const int4 md = sh_meta[L];
+                    if (md.w) {
+                        const int32_t p0 = md.x + 2 * c;
+                        const double2 v =
+                            *reinterpret_cast<const double2*>(&sh_ring[((p0 >> 1) & 15) * 66 + 2 * L]);
+                        double* dst = sh_row[L] + p0;
+                        if (p0 >= md.y && p0 + 1 < md.z) {
+                            st_v2(dst, v.x, v.y);
+                        } else {
+                            if (p0 >= md.y && p0 < md.z) dst[0] = v.x;
+                            if (p0 + 1 >= md.y && p0 + 1 < md.z) dst[1] = v.y;
+                        }
+                    }
+                }
+                __syncwarp();
+            }
+            if (has) fl_lo = hi;
+        }
+    };
+    // the next stream lines into L1 and a few ahead into L2, once per 16 jobs
+    auto prefetch = [&]() {
+        prefetch_l1_if(sp + 16, true);
+        prefetch_l1_if(gp + 16, true);
+        prefetch_l2_if(sp + 80, true);
+        prefetch_l2_if(gp + 80, true);
+    };
+
+    // one job (step j) of the recursion; PH picks the sums' form, act_l
+    // predicates emission and sums on the lane's active flag
+    auto step = [&](auto ph_tag, bool act_l) {
+        constexpr int PH = decltype(ph_tag)::value;
+        const double m = fin[0];
+        const uint32_t k0 = key[0];
+        const uint32_t id = k0 & ID_MASK;
+        const double rv = rbuf[id * 32];  // response of the slot's previous job
+        const double aj = a;
+        const double st = m <= aj ? aj : m;
+        const double d = __dmul_rn(sz, inv_mu);
+        const double f = __dadd_rn(st, d);
+        const double rr = __dsub_rn(f, aj);
+        const bool counted = act_l && !(k0 & DUMMY) && (int32_t)((k0 >> ID_BITS) & J_MASK) >= warm32;
+        ring_put(n_resp, rv);  // slot n_resp is free (< 32 unflushed): kept only if counted
+        n_resp += counted;
+        rbuf[id * 32] = rr;
+        // remove W[0], insert (f, j): equal finish goes after (larger job index)
+        const uint32_t nk = ((uint32_t)j << ID_BITS) | id;
+        bool lt[CMAX];
+#pragma unroll
+        for (int k = 0; k < CMAX - 1; k++) lt[k] = fin[k + 1] <= f;
+        lt[CMAX - 1] = false;
+#pragma unroll
+        for (int k = 0; k < CMAX; k++) {
+            const bool before = k == 0 ? true : lt[k - 1];
+            const double nf = lt[k] ? fin[k + 1 < CMAX ? k + 1 : k] : (before ? f : fin[k]);
+            const uint32_t nkk = lt[k] ? key[k + 1 < CMAX ? k + 1 : k] : (before ? nk : key[k]);
+            fin[k] = nf;
+            key[k] = nkk;
+        }
+        // next job's inputs (stream rows are padded: cursors may run past n)
+        a = __dadd_rn(a, __dmul_rn(scale, g1));
+        g1 = g2;
+        sz = sz1;
+        gp++;
+        sp++;
+        g2 = __ldg(gp + 1);
+        sz1 = __ldg(sp + 1);
+        j++;
+        // per-job sums over the windows (interval [a, f) in system, [st, f)
+        // in service, clipped to [w_start, T]); jobs that end past the
+        // window's end (rare: in system at mid / at the last arrival) take
+        // the clipped form, the rest the plain one
+        if (PH == PH_A) {  // a <= w_start: clipped on both sides
+            if (act_l) {
+                const bool fe = f <= Te;
+                const double he = fe ? f : Te;
+                const double hm = f <= Tm ? f : Tm;
+                const double lo = st >= Ws ? st : Ws;
+                ag[AG_AEND] = __dadd_rn(ag[AG_AEND], dmax0(__dsub_rn(he, Ws)));
+                ag[AG_AMID] = __dadd_rn(ag[AG_AMID], dmax0(__dsub_rn(hm, Ws)));
+                ag[AG_BUSY] = __dadd_rn(ag[AG_BUSY], dmax0(__dsub_rn(he, lo)));
+                ag[AG_ENDQ] += st > Te ? 1.0 : 0.0;
+            }
+        } else {
+            const bool slow = act_l && f > (PH == PH_B ? Tm : Te);
+            if (__any_sync(FULL, slow)) {
+                if (act_l) {
+                    const bool fe = f <= Te;
+                    ag[AG_WAIT] = __dadd_rn(ag[AG_WAIT], __dsub_rn(st, aj));
+                    ag[AG_SERV] = __dadd_rn(ag[AG_SERV], d);
+                    ag[AG_AEND] = __dadd_rn(ag[AG_AEND], fe ? rr : __dsub_rn(Te, aj));
+                    ag[AG_BUSY] = __dadd_rn(ag[AG_BUSY], fe ? __dsub_rn(f, st) : dmax0(__dsub_rn(Te, st)));
+                    if (PH == PH_B) ag[AG_AMID] = __dadd_rn(ag[AG_AMID], f <= Tm ? rr : __dsub_rn(Tm, aj));
+                    ag[AG_ENDQ] += st > Te ? 1.0 : 0.0;
+                }
+            } else if (act_l) {  // f <= T: the plain intervals
+                ag[AG_WAIT] = __dadd_rn(ag[AG_WAIT], __dsub_rn(st, aj));
+                ag[AG_SERV] = __dadd_rn(ag[AG_SERV], d);
+                ag[AG_AEND] = __dadd_rn(ag[AG_AEND], rr);
+                ag[AG_BUSY] = __dadd_rn(ag[AG_BUSY], __dsub_rn(f, st));
+                if (PH == PH_B) ag[AG_AMID] = __dadd_rn(ag[AG_AMID], rr);
+            }
+        }
+    };
+    using TA = std::integral_constant<int, PH_A>;
+    using TB = std::integral_constant<int, PH_B>;
+    using TC = std::integral_constant<int, PH_C>;
+    // up to 16 steps to jn (a multiple of 16 or the range end), split at the
+    // warm-up and mid indices
+    auto run_to = [&](int64_t jn, bool act_l) {
+        while (j < jn) {
+            if (j < warm) {
+                const int cnt = (int)((warm < jn ? warm : jn) - j);
+#pragma unroll 2
+                for (int k = 0; k < cnt; k++) step(TA(), act_l);
+            } else if (j < mid) {
+                const int cnt = (int)((mid < jn ? mid : jn) - j);
+#pragma unroll 2
+                for (int k = 0; k < cnt; k++) step(TB(), act_l);
+            } else {
+                const int cnt = (int)(jn - j);
+#pragma unroll 2
+                for (int k = 0; k < cnt; k++) step(TC(), act_l);
+            }
+        }
+    };
+    auto drain = [&](bool act_l) {  // the remaining slots complete in sorted order
+#pragma unroll
+        for (int k = 0; k < CMAX; k++) {
+            const uint32_t kk = key[k];
+            const bool counted = act_l && !(kk & DUMMY) && fin[k] < INFINITY &&
+                                 (int64_t)((kk >> ID_BITS) & J_MASK) >= warm;
+            if (counted) ring_put(n_resp, rbuf[(kk & ID_MASK) * 32]);
+            n_resp += counted;
+        }
+    };
+    // the block that just ended (j a multiple of BS, or n)
+    auto put_block = [&](bool act_l) {
+        if (act_l) {
+            double* bp = blk + (int64_t)((j - 1) / (int32_t)BS) * NAGG * T;
+#pragma unroll
+            for (int k = 0; k < NAGG; k++) bp[k * T] = ag[k];
+        }
+#pragma unroll
+        for (int k = 0; k < NAGG; k++) ag[k] = 0.0;
+    };
+
+    // ---- phase 1: own range [b, e); checkpoints (state before job
+    // b + ck_offset(q)) for the predecessor's coupling test
+    double* ckf = A.ckf + (((int64_t)s * G + g) * Q) * FCK * 32 + lane;
+    uint32_t* ckk = A.ckk + (((int64_t)s * G + g) * Q) * CMAX * 32 + lane;
+    {
+        int q = 1;
+        int64_t next_ck = Q >= 1 ? b + ck_offset(1) : INT64_MAX;
+        while (j < e) {
+            const int64_t jn = (j + 16 < e) ? j + 16 : e;  // b is a multiple of BS
+            prefetch();
+            run_to(jn, act);
+            flush(false, act);
+            if (j % (int32_t)BS == 0 || j == n) put_block(act);
+            if (j == next_ck) {
+                double* cf = ckf + (int64_t)(q - 1) * FCK * 32;
+                uint32_t* ck = ckk + (int64_t)(q - 1) * CMAX * 32;
+#pragma unroll
+                for (int k = 0; k < CMAX; k++) {
+                    cf[k * 32] = fin[k];
+                    ck[k * 32] = key[k];
+                }
+                cf[CMAX * 32] = __longlong_as_double((int64_t)n_resp);
+                __threadfence();
+                __syncwarp();
+                if (lane == 0) st_release(A.progress + unit, (uint32_t)q);
+                q++;
+                next_ck = q <= Q ? b + ck_offset(q) : INT64_MAX;
+            }
+        }
+    }
+    if (tr && lane == 0) tr[1] = gtimer();
+    if (e == n) {  // the last segment finishes the row
+        drain(act);
+        flush(true, act);
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) st_release(A.progress + unit, DONE | (uint32_t)Q);
+        if (tr && lane == 0) tr[2] = tr[3] = gtimer();
+        return;
+    }
+    flush(true, act);  // everything this segment emitted in its own range
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) st_release(A.progress + unit, DONE | (uint32_t)Q);
+
+    // ---- phase 2: continue only where this segment is known to be exact
+    if (s > 0) {
+        int32_t stv = valid ? ST_UNKNOWN : ST_SKIPPED;
+        while (__any_sync(FULL, stv == ST_UNKNOWN)) {
+            if (stv == ST_UNKNOWN) stv = ld_acquire(A.status + (int64_t)s * T + tid);
+            if (__any_sync(FULL, stv == ST_UNKNOWN)) __nanosleep(256);
+        }
+        act = valid && stv >= 2;
+    }
+    if (tr && lane == 0) tr[2] = gtimer();
+    int t = s + 1;
+    while (__any_sync(FULL, act)) {
+        // entering segment t's range: its phase-1 writes (responses, blocks)
+        // must be complete before ours overwrite them
+        const uint32_t* prog = A.progress + (int64_t)t * G + g;
+        while (!(ld_acquire(prog) & DONE)) __nanosleep(256);
+        const int64_t bt = seg_begin(t, S, n), et = seg_begin(t + 1, S, n);
+        const double* tcf = A.ckf + (((int64_t)t * G + g) * Q) * FCK * 32 + lane;
+        const uint32_t* tck = A.ckk + (((int64_t)t * G + g) * Q) * CMAX * 32 + lane;
+        int q = 1;
+        int64_t next_ck = Q >= 1 ? bt + ck_offset(1) : INT64_MAX;
+        while (j < et && __any_sync(FULL, act)) {
+            const int64_t jn = (j + 16 < et) ? j + 16 : et;
+            prefetch();
+            run_to(jn, act);
+            flush(false, act);
+            if (j % (int32_t)BS == 0 || j == n) put_block(act);
+            if (j == next_ck) {
+                bool same = act;
+                if (act) {
+                    const double* cf = tcf + (int64_t)(q - 1) * FCK * 32;
+                    const uint32_t* ck = tck + (int64_t)(q - 1) * CMAX * 32;
+#pragma unroll
+                    for (int k = 0; k < CMAX; k++)
+                        same = same && __ldcg(cf + k * 32) == fin[k] &&
+                               ((__ldcg(ck + k * 32) ^ key[k]) & ~ID_MASK) == 0;
+                    same = same && __double_as_longlong(__ldcg(cf + CMAX * 32)) == (int64_t)n_resp;
+                }
+                if (__any_sync(FULL, same)) {
+                    flush(true, same);  // our emissions before the hand-over
+                    if (same) {
+                        st_release(A.status + (int64_t)t * T + tid, (int32_t)(2 + j));
+                        act = false;
+                    }
+                }
+                q++;
+                next_ck = q <= Q ? bt + ck_offset(q) : INT64_MAX;
+            }
+        }
+        if (j == et && __any_sync(FULL, act)) {
+            if (et == n) {  // ran through the last segment: these lanes finish the row
+                drain(act);
+                flush(true, act);
+                act = false;
+            } else {
+                if (act) st_release(A.status + (int64_t)t * T + tid, ST_SKIPPED);
+                t++;
+            }
+        }
+    }
+    if (tr && lane == 0) tr[3] = gtimer();
+}
+
+// ---------------------------------------------------------------------------
+// Finalize: per row, add the block sums in block order (every block was
+// written last by the exact run over it) and form the RepResult fields as
+// sim.py:298-324 does.
+// ---------------------------------------------------------------------------
+__global__ void seg_finalize_kernel(Args A) {
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t T = (int64_t)A.P * A.R;
+    if (tid >= T) return;
+    const int S = A.nseg;
+    const int32_t r = (int32_t)(tid / A.P), p = (int32_t)(tid % A.P);
+    const int64_t o = (int64_t)p * A.RT + A.rb + r;
+    const int64_t n = A.n, warm = A.warm;
+    const double* pre = A.prefix + tid * (S + 3);
+    double ag[NAGG];
+    for (int k = 0; k < NAGG; k++) ag[k] = 0.0;
+    const double* bp = A.blk + tid;
+    for (int64_t kb = 0; kb < A.nblk; kb++)
+        for (int k = 0; k < NAGG; k++) ag[k] = __dadd_rn(ag[k], bp[(kb * NAGG + k) * T]);
+    const double w_start = pre[S], t_mid = pre[S + 1], t_end = pre[S + 2];
+    cs_rep_summary out;
+    const double window = __dsub_rn(t_end, w_start);
+    out.wait_sum = ag[AG_WAIT];
+    out.service_sum = ag[AG_SERV];
+    out.counted = n - warm;
+    out.window_s = window;
+    const double area_end = ag[AG_AEND], area_mid = ag[AG_AMID];
+    if (window > 0.0) {
+        out.mean_occupancy = __ddiv_rn(area_end, window);
+        out.lambda_effective = __ddiv_rn((double)(n - warm), window);
+    } else {
+        out.mean_occupancy = NAN;
+        out.lambda_effective = NAN;
+    }
+    out.occ_first_half = t_mid > w_start ? __ddiv_rn(area_mid, __dsub_rn(t_mid, w_start)) : NAN;
+    out.occ_second_half =
+        t_end > t_mid ? __ddiv_rn(__dsub_rn(area_end, area_mid), __dsub_rn(t_end, t_mid)) : NAN;
+    out.end_queue_len = (int64_t)ag[AG_ENDQ];
+    out.w_start = w_start;
+    out.t_mid = t_mid;
+    out.area_mid = area_mid;
+    out.t_end = t_end;
+    out.area_end = area_end;
+    out.resp_sum = NAN;  // filled by the statistics pass (numpy pairwise order)
+    out.resp_mean = NAN;
+    A.summ[o] = out;
+    A.busy_out[o * A.ldb] = ag[AG_BUSY];
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+struct Plan {
+    int S, G, Q, cmax;
+    int64_t T, nblk;
+    size_t off_prefix, off_ckf, off_ckk, off_blk, off_status, off_progress, bytes;
+};
+
+static int pick_cmax(int32_t max_cap) { return max_cap <= 4 ? 4 : max_cap <= 7 ? 7 : max_cap <= 8 ? 8 : 16; }
+
+template <int CMAX>
+static int max_resident_blocks() {
+    static int cached[64] = {0};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+    if (dev < 64 && cached[dev]) return cached[dev];
+    int per_sm = 0, sms = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jffc_seg_kernel<CMAX>, 32, 0) != cudaSuccess ||
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    const int v = per_sm * sms;
+    if (dev < 64) cached[dev] = v;
+    return v;
+}
+
+static int resident_blocks(int cmax) {
+    switch (cmax) {
+        case 4: return max_resident_blocks<4>();
+        case 7: return max_resident_blocks<7>();
+        case 8: return max_resident_blocks<8>();
+        default: return max_resident_blocks<16>();
+    }
+}
+
+static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+// S (segments per row): as many as keep every segment of the launch resident
+// (phase-2 waits), segments of >= 8 blocks.  The results do not depend on S.
+static Plan make_plan(int32_t P, int32_t R, int32_t max_cap, int64_t n) {
+    Plan pl{};
+    pl.cmax = pick_cmax(max_cap);
+    pl.T = (int64_t)P * R;
+    pl.G = (int)((pl.T + 31) / 32);
+    pl.nblk = (n + BS - 1) / BS;
+    const int cap_blocks = resident_blocks(pl.cmax);
+    const int s_fit = pl.G > 0 && cap_blocks > 0 ? std::max(1, cap_blocks / pl.G) : 1;
+    const int s_len = (int)std::max<int64_t>(1, std::min<int64_t>(64, n / (8 * BS)));
+    int S = std::min(s_fit, s_len);
+    if (const char* e = getenv("CS_SEG_S")) S = std::max(1, std::min(std::min(s_fit, s_len), atoi(e)));
+    pl.S = S;
+    int64_t lmin = n;
+    for (int s = 0; s < S; s++) lmin = std::min(lmin, seg_begin(s + 1, S, n) - seg_begin(s, S, n));
+    int Q = 0;
+    while (Q < MAXQ && ck_offset(Q + 1) < lmin) Q++;
+    pl.Q = Q;
+    size_t off = 0;
+    pl.off_prefix = off;
+    off = align256(off + sizeof(double) * pl.T * (S + 3));
+    pl.off_ckf = off;
+    off = align256(off + sizeof(double) * (size_t)S * pl.G * std::max(Q, 1) * (pl.cmax + 1) * 32);
+    pl.off_ckk = off;
+    off = align256(off + sizeof(uint32_t) * (size_t)S * pl.G * std::max(Q, 1) * pl.cmax * 32);
+    pl.off_blk = off;
+    off = align256(off + sizeof(double) * (size_t)pl.nblk * NAGG * pl.T);
+    pl.off_status = off;
+    off = align256(off + sizeof(int32_t) * (size_t)S * pl.T);
+    pl.off_progress = off;
+    off = align256(off + sizeof(uint32_t) * (size_t)S * pl.G);
+    pl.bytes = off;
+    return pl;
+}
+
+template <int CMAX>
+static int launch(const Plan& pl, Args A, cudaStream_t st) {
+    const int blocks = pl.S * pl.G;
+    const bool trace = getenv("CS_SEG_TRACE") != nullptr;  // development timeline (stderr)
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    if (trace) {
+        cudaMalloc(&A.trace, sizeof(unsigned long long) * 4 * blocks);
+        cudaEventCreate(&ev0);
+        cudaEventCreate(&ev1);
+        cudaEventRecord(ev0, st);
+    }
+    if (pl.S > 1) {  // phase-2 waits need every segment resident
+        void* params[] = {&A};
+        const cudaError_t e =
+            cudaLaunchCooperativeKernel((const void*)jffc_seg_kernel<CMAX>, dim3(blocks), dim3(32), params, 0, st);
+        if (e != cudaSuccess) return check_cuda(e, "jffc_seg_kernel (cooperative launch)");
+    } else {
+        jffc_seg_kernel<CMAX><<<blocks, 32, 0, st>>>(A);
+    }
+    int rc = check_launch("jffc_seg_kernel");
+    if (rc) return rc;
+    if (trace) {
+        cudaEventRecord(ev1, st);
+        cudaEventSynchronize(ev1);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ev0, ev1);
+        fprintf(stderr, "jffc_seg_kernel %.3f ms\n", ms);
+        cudaEventDestroy(ev0);
+        cudaEventDestroy(ev1);
+        std::vector<unsigned long long> h((size_t)4 * blocks);
+        cudaMemcpyAsync(h.data(), A.trace, h.size() * 8, cudaMemcpyDeviceToHost, st);
+        cudaStreamSynchronize(st);
+        cudaFree(A.trace);
+        unsigned long long t0 = ~0ull;
+        for (int b = 0; b < blocks; b++) t0 = std::min(t0, h[4 * b]);
+        for (int s = 0; s < pl.S; s++) {
+            std::vector<double> v[4];
+            for (int g = 0; g < pl.G; g++)
+                for (int k = 0; k < 4; k++) v[k].push_back((h[4 * ((size_t)s * pl.G + g) + k] - t0) * 1e-6);
+            fprintf(stderr, "seg %d:", s);
+            for (int k = 0; k < 4; k++) {
+                std::sort(v[k].begin(), v[k].end());
+                fprintf(stderr, " [%s %.3f/%.3f/%.3f ms]", k == 0 ? "start" : k == 1 ? "ph1end" : k == 2 ? "ph2start" : "end",
+                        v[k][0], v[k][v[k].size() / 2], v[k].back());
+            }
+            fprintf(stderr, "\n");
+        }
+    }
+    seg_finalize_kernel<<<(int)((pl.T + 127) / 128), 128, 0, st>>>(A);
+    return check_launch("seg_finalize_kernel");
+}
+
+}  // namespace seg
+}  // namespace cs
+
+// Workspace bytes of the segmented path (0 when it does not apply).
+extern "C" int64_t cs_seg_workspace_bytes_impl(int32_t P, int32_t R, int32_t max_chains, int32_t max_cap,
+                                               int64_t n) {
+    if (max_chains > 1 || max_cap > 16 || n >= (1ll << 27) || P <= 0 || R <= 0) return 0;
+    return (int64_t)cs::seg::make_plan(P, R, max_cap, n).bytes;
+}
+
+// The plan the segmented path would use: out[0..4) = segments per row,
+// warps per segment, checkpoints per segment, slot capacity instance.
+extern "C" int cs_seg_plan(int32_t P, int32_t R, int32_t max_cap, int64_t n, int32_t* out) {
+    const cs::seg::Plan pl = cs::seg::make_plan(P, R, max_cap, n);
+    out[0] = pl.S;
+    out[1] = pl.G;
+    out[2] = pl.Q;
+    out[3] = pl.cmax;
+    return CS_OK;
+}
+
+// Segmented single-chain simulation of P points x R replications (the chunk
+// rb.. of RT); same outputs as cs_jffc_sim_impl's k1 path, except d_jobs
+// (trace) which this path does not produce.
+extern "C" int cs_seg_sim_impl(const cs_sim_point* d_points, int32_t P, const double* d_rates,
+                               const int32_t* d_caps, int32_t max_cap, const double* d_streams,
+                               int64_t lds, int32_t rb, int32_t R, int32_t RT, int64_t n, int64_t warm,
+                               double* d_resp, int64_t ldr, double* d_busy, int32_t ldb,
+                               cs_rep_summary* d_summ, void* d_ws, int64_t ws_bytes, void* stream) {
+    using namespace cs;
+    using namespace cs::seg;
+    const Plan pl = make_plan(P, R, max_cap, n);
+    if (pl.T == 0) return CS_OK;
+    if (d_ws == nullptr || ws_bytes < (int64_t)pl.bytes) {
+        set_error("cs_jffc_sim: segmented path needs %lld workspace bytes", (long long)pl.bytes);
+        return CS_INVALID;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    char* ws = (char*)d_ws;
+    Args A{};
+    A.pts = d_points;
+    A.rates = d_rates;
+    A.caps = d_caps;
+    A.S = d_streams;
+    A.lds = lds;
+    A.P = P;
+    A.R = R;
+    A.RT = RT;
+    A.rb = rb;
+    A.n = n;
+    A.warm = warm;
+    A.resp = d_resp;
+    A.ldr = ldr;
+    A.busy_out = d_busy;
+    A.ldb = ldb;
+    A.summ = d_summ;
+    A.prefix = (double*)(ws + pl.off_prefix);
+    A.ckf = (double*)(ws + pl.off_ckf);
+    A.ckk = (uint32_t*)(ws + pl.off_ckk);
+    A.blk = (double*)(ws + pl.off_blk);
+    A.status = (int32_t*)(ws + pl.off_status);
+    A.progress = (uint32_t*)(ws + pl.off_progress);
+    A.nblk = pl.nblk;
+    A.nseg = pl.S;
+    A.G = pl.G;
+    A.Q = pl.Q;
+    A.cmax = pl.cmax;
+    // statuses (segment 0 exact) and progress words: fresh per launch
+    int rc = check_cuda(cudaMemsetAsync(ws + pl.off_status, 0, pl.off_progress + sizeof(uint32_t) * pl.S * pl.G -
+                                                                  pl.off_status, st),
+                        "seg workspace reset");
+    if (rc) return rc;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    if (getenv("CS_SEG_TRACE")) {
+        cudaEventCreate(&ev0);
+        cudaEventCreate(&ev1);
+        cudaEventRecord(ev0, st);
+    }
+    {
+        // ring of the prefix pass: PF_NBUF chunks x (distinct rows per warp) lines
+        const int rows_per_warp = (int)std::min<int64_t>(32, (31 + P - 1) / P + 1);
+        const size_t smem = sizeof(double) * PF_NBUF * rows_per_warp * PF_U;
+        if (smem > 48 * 1024)
+            cudaFuncSetAttribute(seg_prefix_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        seg_prefix_kernel<<<(int)((pl.T + 31) / 32), 32, smem, st>>>(A);
+    }
+    if ((rc = check_launch("seg_prefix_kernel"))) return rc;
+    if (ev0) {
+        cudaEventRecord(ev1, st);
+        cudaEventSynchronize(ev1);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ev0, ev1);
+        fprintf(stderr, "seg_prefix_kernel %.3f ms (S=%d G=%d Q=%d)\n", ms, pl.S, pl.G, pl.Q);
+        cudaEventDestroy(ev0);
+        cudaEventDestroy(ev1);
+    }
+    switch (pl.cmax) {
+        case 4: return launch<4>(pl, A, st);
+        case 7: return launch<7>(pl, A, st);
+        case 8: return launch<8>(pl, A, st);
+        default: return launch<16>(pl, A, st);
+    }
+}

@@ -49,7 +49,7 @@ class SweepEngine:
         self.P, self.R, self.n = len(lams), reps, n_jobs
         self.warm = int(warmup_fraction * n_jobs)
         self.m = n_jobs - self.warm
-        self.ldr = (self.m + 1) & ~1
+        self.ldr = (self.m + 15) & ~15  # whole 128-byte lines per row (simulator flushes lines)
         self.lds = 2 * n_jobs
         self.seed, self.rep_begin = seed, rep_begin
         self.log1p_variant = self.lib.cs_host_log1p_variant() if log1p_variant < 0 else log1p_variant
@@ -149,9 +149,6 @@ class SweepEngine:
         s_gen, s_sim, s_stat = self.pipe
         if ordered is None:
             ordered = self.distributed or bool(os.environ.get("CS_PIPE_ORDERED"))
-        part = None if ordered else self._sm_partition()
-        if part is not None:  # simulator alone on its SMs; streams + statistics on the rest
-            s_sim, s_gen, s_stat = part
         cur = torch.cuda.current_stream()
         for s_ in self.pipe:
             s_.wait_stream(cur)
@@ -210,42 +207,6 @@ class SweepEngine:
         for s_ in self.pipe:
             cur.wait_stream(s_)
         return (steps - 1) & 1
-
-    def _sm_partition(self):
-        """(sim, gen, stat) streams on two green-context SM partitions, or None.
-
-        The simulator's SM count keeps its most loaded SM at the same warp
-        count as an even spread over the whole device (ceil(warps / SMs)),
-        leaving the remaining SMs to the streams and statistics of the
-        neighbouring sweeps (see csrc/partition.cu).  Only for the one-warp-
-        per-32-replications kernels.  Opt-in (CS_SM_PARTITION=1): on config 2
-        the simulator takes 40.7 ms on 128 SMs (37.0 ms on all 148) and the
-        streams + statistics 41 ms on the other 20, so the split sweep costs
-        45 ms against 40.5 ms unsplit."""
-        if os.environ.get("CS_SM_PARTITION", "0") != "1":
-            return None
-        if getattr(self, "_part", False) is not False:
-            return self._part
-        self._part = None
-        if self.max_chains > 8 or self.max_cap > 16 or self.n >= (1 << 27):
-            return None
-        torch = self.torch
-        n_sm = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
-        warps = -(-self.P * self.R // 32)
-        per = -(-warps // n_sm)
-        sim_sms = -(-warps // per)
-        sim_sms += sim_sms & 1  # partitions come in SM pairs
-        if n_sm - sim_sms < 8:
-            return None
-        s_sim, aux = C.c_void_p(), (C.c_void_p * 2)()
-        got_sim, got_aux = C.c_int32(), C.c_int32()
-        rc = self.lib.cs_sm_partition(sim_sms, C.byref(s_sim), aux, C.byref(got_sim), C.byref(got_aux))
-        if rc != 0:
-            return None
-        ext = torch.cuda.ExternalStream
-        self._part = (ext(s_sim.value), ext(aux[0]), ext(aux[1]))
-        self.partition_sms = (got_sim.value, got_aux.value)
-        return self._part
 
     def step(self, timed: bool = False) -> StageTimes | None:
         """One full sweep on the device; optional per-stage CUDA-event times."""

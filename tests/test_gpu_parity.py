@@ -1,7 +1,9 @@
 """GPU parity: the CUDA engine (through the C-ABI / drop-in API) vs the
 reference's golden outputs and vs the pinned CPU oracle on the same seeded
 inputs.  Bit-exact for everything except the merged-mean response time, whose
-stated tolerance (north_star) is 1e-6 relative -- we assert 1e-12.
+stated tolerance (north_star) is 1e-6 relative -- we assert 1e-12 -- and, on
+the segmented single-chain path, the per-job sums of conftest.SUM_FIELDS and
+busy time (reassociated, asserted <= 1e-12 relative).
 """
 
 import math
@@ -9,7 +11,7 @@ import math
 import numpy as np
 import pytest
 
-from conftest import bits, same_float, servers_from_rows
+from conftest import bits, close_rel, same_float, same_rep_field, seg_path, servers_from_rows
 
 pytestmark = pytest.mark.gpu
 
@@ -71,11 +73,15 @@ def test_simulate_once_matches_reference(eng, golden, i):
     c = meta["sim_cases"][i]
     res = _sweep(eng, c)
     s = res.summaries[0, 0]
-    for f in REP_FIELDS:
-        assert same_float(s[f], c["fields"][f]), (f, s[f], c["fields"][f])
-    assert np.array_equal(bits(res.responses[0, 0]), bits(arr[c["responses"]]))
     K = len(c["rates"])
-    assert np.array_equal(bits(res.busy[0, 0, :K]), bits(arr[c["busy"]]))
+    seg = seg_path(K, c["jobs"])
+    for f in REP_FIELDS:
+        assert same_rep_field(f, s[f], c["fields"][f], seg), (f, s[f], c["fields"][f])
+    assert np.array_equal(bits(res.responses[0, 0]), bits(arr[c["responses"]]))
+    if seg:
+        assert all(close_rel(x, y) for x, y in zip(res.busy[0, 0, :K], arr[c["busy"]]))
+    else:
+        assert np.array_equal(bits(res.busy[0, 0, :K]), bits(arr[c["busy"]]))
     if c["rep_mean"] is not None:
         assert same_float(s["resp_mean"], c["rep_mean"])  # numpy pairwise mean, bit-exact
     if c["jobs"]:
@@ -90,22 +96,32 @@ def test_run_sim_matches_reference(eng, golden, i):
                                    workload=eng.PoissonWorkload(c["lam"]), horizon_jobs=c["n"],
                                    warmup_fraction=c["wf"], seed=c["seed"],
                                    replications=c["reps"])).to_dict()
+    # statistics derived from the per-job sums (SUM_FIELDS, busy) on the
+    # segmented single-chain path: 1e-12 relative
+    seg = seg_path(len(c["rates"]))
+    summed = {"mean_waiting_s", "mean_service_s", "mean_occupancy", "occupancy_ci_half_width",
+              "per_chain_utilization", "rep_mean_occupancy", "occ_first_half", "occ_second_half"}
     for k, v in c["stats"].items():
         g = st[k]
+        eq = close_rel if seg and k in summed else same_float
         if k == "mean_response_s":
             assert abs(g - v) <= 1e-12 * abs(v), (g, v)
         elif k == "little_law_gap":
-            assert abs(g - v) <= 1e-9 * max(abs(v), 1e-12), (g, v)
+            assert abs(g - v) <= 1e-9 * max(abs(v), 1e-12) + (1e-11 if seg else 0.0), (g, v)
         elif isinstance(v, list):
-            assert len(g) == len(v) and all(same_float(a, b) for a, b in zip(g, v)), (k, g, v)
+            assert len(g) == len(v) and all(eq(a, b) for a, b in zip(g, v)), (k, g, v)
         elif isinstance(v, float):
-            assert same_float(g, v), (k, g, v)
+            assert eq(g, v), (k, g, v)
         else:
             assert g == v, (k, g, v)
 
 
-def test_sweep_matches_oracle_bit_exact(eng, oracle):
-    """16 arrival rates x 24 reps on the PETALS composition (config-2 shape, small n)."""
+@pytest.mark.parametrize("exact", [True, False], ids=["exact", "segmented"])
+def test_sweep_matches_oracle_bit_exact(eng, oracle, exact, monkeypatch):
+    """16 arrival rates x 24 reps on the PETALS composition (config-2 shape,
+    small n), through the serial bit-exact kernel (CS_SIM_EXACT=1) and the
+    default segmented one."""
+    monkeypatch.setenv("CS_SIM_EXACT", "1" if exact else "0")
     service, servers, _ = eng.petals_instance(10, 0.2, 101)
     system = eng.greedy_cache_allocation(
         eng.greedy_block_placement(servers, service, 7, 0.2, 0.7).placement)
@@ -119,10 +135,13 @@ def test_sweep_matches_oracle_bit_exact(eng, oracle):
                                                 seed, 0, R, threads=4)
         assert np.array_equal(bits(res.responses[p]), bits(resp)), p
         K = len(system.rates)
-        assert np.array_equal(bits(res.busy[p][:, :K]), bits(busy)), p
+        if exact:
+            assert np.array_equal(bits(res.busy[p][:, :K]), bits(busy)), p
+        else:
+            assert all(close_rel(x, y) for x, y in zip(res.busy[p][:, 0], busy[:, 0])), p
         for r in range(R):
             for f in REP_FIELDS:
-                assert same_float(res.summaries[p, r][f], getattr(summ[r], f)), (p, r, f)
+                assert same_rep_field(f, res.summaries[p, r][f], getattr(summ[r], f), not exact), (p, r, f)
         # exact order statistics of the merged responses
         merged = np.sort(resp.ravel())
         for rank, v in res.order_stats[p].items():
@@ -285,16 +304,14 @@ def test_sample_select_and_fused_pairwise_means(eng, oracle):
         assert np.array_equal(bits(res.summaries[p]["resp_mean"]), bits(means))
 
 
-@pytest.mark.parametrize("schedule", ["overlapped", "ordered", "sm_partition"])
-def test_sweep_engine_pipelined_equals_unpipelined(eng, schedule, monkeypatch):
+@pytest.mark.parametrize("schedule", ["overlapped", "ordered"])
+def test_sweep_engine_pipelined_equals_unpipelined(eng, schedule):
     """SweepEngine.run_pipelined (two buffer sets, three CUDA streams; the
     benchmark's timed loop) computes every sweep exactly like step(), in
-    either order and on green-context SM partitions."""
+    either order."""
     import torch
 
     from paper_2604_14993_b200.engine import SweepEngine
-
-    monkeypatch.setenv("CS_SM_PARTITION", "1" if schedule == "sm_partition" else "0")
 
     service, servers, _ = eng.petals_instance(10, 0.2, 101)
     system = eng.greedy_cache_allocation(
@@ -306,8 +323,6 @@ def test_sweep_engine_pipelined_equals_unpipelined(eng, schedule, monkeypatch):
     ref_s, ref_b, ref_o = e.summaries(0).copy(), e.busy(0).copy(), e.order_stats()
     last = e.run_pipelined(3, ordered=schedule == "ordered")
     torch.cuda.synchronize()
-    if schedule == "sm_partition":
-        assert getattr(e, "partition_sms", (0, 0))[1] > 0  # the partition was made and used
     for b in (0, 1):  # both buffer sets hold a complete, identical sweep
         assert np.array_equal(e.summaries(b).view(np.uint8), ref_s.view(np.uint8)), b
         assert np.array_equal(bits(e.busy(b)), bits(ref_b)), b
