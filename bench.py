@@ -7,9 +7,15 @@ blocks, 10 heterogeneous servers; reference fixture wan_gpu_fixture(10, 0.2,
 capacity 7, nu=0.5165/s), then 16 arrival rates lambda_i = nu*linspace(0.05,
 0.95, 16) x 1024 seed replications (seed=1, spawn_key=(r,)) x 1e5 jobs,
 warm-up 0.1: 1.6384e9 simulated jobs per step.  A step = numpy-exact Philox
-exponential streams -> JFFC event simulation -> per-rep means + exact
-quantiles, all on the GPU.  The stored responses (11.8 GB) exceed L2 126 MB,
-so no flush is needed between steps.
+exponential streams -> JFFC simulation (segmented single-chain kernel) ->
+per-rep means + exact quantiles, all on the GPU.  The stored responses (11.8
+GB) exceed L2 126 MB, so no flush is needed between steps.
+
+The same line carries, as sub-objects: the simulator's issue roofline with the
+RNG-floor and HBM fractions, config 5's share (8192 replications x 1e6 jobs
+split over the N GPUs: strong scaling across the driver's N=1,2,4,8 runs),
+config 4's composed instances/s in both lambda regimes, and the reference's
+own CPU run_sim timed on this host beside the C port.
 
     python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 
@@ -49,6 +55,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--cpu-sample-reps", type=int, default=128)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-config5", action="store_true")
+    ap.add_argument("--no-compose", action="store_true")
     return ap.parse_args()
 
 
@@ -127,6 +135,8 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
+
+
 def measured_peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(path):
@@ -136,88 +146,207 @@ def measured_peaks():
     return 6650.0, "fallback"
 
 
-def ncu_traffic(kernel: str, jobs: int, reps: int, points: int):
-    """DRAM bytes per launch of `kernel` from the committed ncu capture (same config only)."""
-    path = os.path.join(ROOT, "profiles", "r1_traffic.json")
-    if not os.path.exists(path) or (jobs, reps, points) != (100_000, 1024, 16):
+NCU_SUMMARY = os.path.join(ROOT, "profiles", "r2_ncu_summary.json")
+
+
+def ncu_summary(jobs: int, reps: int, points: int):
+    """Per-launch ncu counters of the kernels (committed capture of this same
+    config: instructions, DRAM bytes, issue-slot utilisation), or None."""
+    if not os.path.exists(NCU_SUMMARY):
         return None
-    with open(path) as fh:
-        k = json.load(fh)["kernels"].get(kernel)
-    return None if k is None else int(k["dram_read_bytes"] + k["dram_write_bytes"])
+    with open(NCU_SUMMARY) as fh:
+        d = json.load(fh)
+    if tuple(d.get("shape", ())) != (points, reps, jobs):
+        return None
+    return d
 
 
-def sim_kernel_name(K: int, C: int, jobs: int) -> str:
-    """The simulator kernel cs_jffc_sim dispatches to (jffc_sim.cu:sim_path)."""
-    if K == 1 and C <= 16:
-        return "jffc_sim_k1_kernel"
-    return "jffc_sim_reg_kernel" if K <= 8 and C <= 16 else "jffc_sim_warp_kernel"
+# ---------------------------------------------------------------------------
+# The reference itself (pure Python, installed unmodified into baseline/_ref:
+# pip install --no-deps --target baseline/_ref <copy of /root/reference/pkg>)
+# ---------------------------------------------------------------------------
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
 
 
-def cpu_baseline(rates, caps, lams, args, reps=None):
-    """The oracle port (C, all host threads) on a bounded sample of the workload."""
+def reference_pkg():
+    if not os.path.isdir(os.path.join(REF_DIR, "chainserve")):
+        return None
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    import chainserve
+
+    return chainserve
+
+
+def reference_composition(cs):
+    """config-2 composition with the reference's own greedy_block_placement +
+    greedy_cache_allocation (PETALS fixture built by this package's
+    petals_instance, converted to the reference's dataclasses)."""
+    import paper_2604_14993_b200 as P
+
+    service, servers, _ = P.petals_instance(10, 0.2, 101)
+    rsvc = cs.ServiceSpec(service.block_count, service.block_bytes, service.cache_slot_bytes)
+    rsrv = tuple(cs.ServerSpec(s.id, s.memory_bytes, s.comm_time_s, s.per_block_compute_s) for s in servers)
+    placed = cs.greedy_block_placement(rsrv, rsvc, 7, 0.2, 0.7)
+    system = cs.greedy_cache_allocation(placed.placement)
+    return tuple(1.0 / ch.service_time_s for ch in system.chains), tuple(system.capacities)
+
+
+def reference_run_sim_time(cs, rates, caps, lam, jobs, reps, workers):
+    """Seconds of the reference's run_sim (process pool over replications) on one sample."""
+    cfg = cs.SimConfig(rates=rates, capacities=caps, workload=cs.PoissonWorkload(lam), horizon_jobs=jobs,
+                       warmup_fraction=0.1, seed=1, replications=reps, workers=workers)
+    t0 = time.perf_counter()
+    cs.run_sim(cfg)
+    return time.perf_counter() - t0
+
+
+def cpu_baseline(rates, caps, lams, args):
+    """CPU figures on this host: the reference's own run_sim (workers = cores,
+    when baseline/_ref is installed) on a stated sample, and the C port of
+    sim.py (oracle/cs_oracle.c, all host threads) on a larger one."""
     from oracle import oracle as O
 
     O.build()
-    reps = reps or args.cpu_sample_reps
-    threads = os.cpu_count() or 1
+    cores = os.cpu_count() or 1
+    reps = args.cpu_sample_reps
     jobs = 0
     t0 = time.perf_counter()
     for lam in lams:
-        O.simulate_reps(rates, caps, lam, args.jobs, 0.1, 1, 0, reps, threads=threads)
+        O.simulate_reps(rates, caps, lam, args.jobs, 0.1, 1, 0, reps, threads=cores)
         jobs += reps * args.jobs
     dt = time.perf_counter() - t0
-    return {"value": jobs / dt, "unit": "jobs/s", "cores": threads, "kind": "port",
+    port = {"value": jobs / dt, "unit": "jobs/s", "cores": cores, "kind": "port",
             "sample": f"{len(lams)} lambdas x {reps} reps x {args.jobs} jobs = {jobs:.3g} jobs "
-                      f"(oracle/cs_oracle.c, {threads} threads) in {dt:.2f} s"}
+                      f"(oracle/cs_oracle.c, {cores} threads) in {dt:.2f} s"}
+    cs = reference_pkg()
+    if cs is None:
+        return port
+    lam = lams[len(lams) // 2]
+    rdt = reference_run_sim_time(cs, rates, caps, lam, args.jobs, cores, cores)
+    return {"value": cores * args.jobs / rdt, "unit": "jobs/s", "cores": cores, "kind": "reference",
+            "sample": f"chainserve.run_sim (baseline/_ref, unmodified reference) lambda={lam:.4g}, "
+                      f"{cores} replications x {args.jobs} jobs, workers={cores}, in {rdt:.2f} s",
+            "port": port}
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the CPU implementation (oracle port; the reference itself is
-    Python and absent on the GPU box) on the host cores, same metric/config."""
+    """--impl reference: the reference's own CPU implementation (chainserve
+    run_sim from baseline/_ref, workers = host cores) on this host, on the
+    engine arm's config 2 composition and lambda grid; each step simulates
+    `cores` replications x 1e5 jobs of one lambda of the grid (cycling).  The
+    C port (oracle/) stands in only when baseline/_ref is absent."""
     if rank != 0:
         return
-    service, servers = workload(args)
-    # the composition is an input of the timed path; compose it with the oracle (CPU)
-    from oracle import oracle as O
+    cores = os.cpu_count() or 1
+    cs = reference_pkg()
+    if cs is not None:
+        rates, caps = reference_composition(cs)
+        kind = "reference"
+    else:
+        from oracle import oracle as O
 
-    O.build()
-    ids = [s.id for s in servers]
-    st, g = O.gbp([s.memory_bytes for s in servers], [s.comm_time_s for s in servers],
-                  [s.per_block_compute_s for s in servers], ids, service.block_count,
-                  service.block_bytes, service.cache_slot_bytes, 7, 0.2, 0.7)
-    st, a = O.gca([s.memory_bytes for s in servers], [s.comm_time_s for s in servers],
-                  [s.per_block_compute_s for s in servers], ids, service.block_count,
-                  service.block_bytes, service.cache_slot_bytes, g["first"], g["count"])
-    rates = tuple(1.0 / t for t in a["times"])
-    caps = tuple(int(c) for c in a["caps"])
+        O.build()
+        service, servers = workload(args)
+        ids = [s.id for s in servers]
+        mem = [s.memory_bytes for s in servers]
+        tc = [s.comm_time_s for s in servers]
+        tp = [s.per_block_compute_s for s in servers]
+        st, g = O.gbp(mem, tc, tp, ids, service.block_count, service.block_bytes, service.cache_slot_bytes,
+                      7, 0.2, 0.7)
+        st, a = O.gca(mem, tc, tp, ids, service.block_count, service.block_bytes, service.cache_slot_bytes,
+                      g["first"], g["count"])
+        rates, caps = tuple(1.0 / t for t in a["times"]), tuple(int(c) for c in a["caps"])
+        kind = "port"
     lams, _ = lam_grid(rates, caps, args.points)
-    sample_reps = max(1, min(16, args.reps))
-    threads = os.cpu_count() or 1
-    for _ in range(args.warmup):
-        O.simulate_reps(rates, caps, lams[0], args.jobs, 0.1, 1, 0, min(threads, sample_reps), threads)
-    t0 = time.perf_counter()
-    jobs = 0
-    for _ in range(args.steps):
-        for lam in lams:
-            O.simulate_reps(rates, caps, lam, args.jobs, 0.1, 1, 0, sample_reps, threads=threads)
-            jobs += sample_reps * args.jobs
-    dt = time.perf_counter() - t0
+
+    def one(lam):
+        if cs is not None:
+            return reference_run_sim_time(cs, rates, caps, lam, args.jobs, cores, cores)
+        t0 = time.perf_counter()
+        O.simulate_reps(rates, caps, lam, args.jobs, 0.1, 1, 0, cores, threads=cores)
+        return time.perf_counter() - t0
+
+    for k in range(args.warmup):
+        one(lams[k % len(lams)])
+    dt = sum(one(lams[k % len(lams)]) for k in range(args.steps))
+    jobs = args.steps * cores * args.jobs
     value = jobs / dt
+    sample = (f"{cores} replications x {args.jobs} jobs per step (lambda cycling over the "
+              f"{args.points}-point grid), " +
+              (f"chainserve.run_sim from baseline/_ref (unmodified reference), workers={cores}"
+               if kind == "reference" else f"oracle/cs_oracle.c port, {cores} threads"))
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "jobs/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "config": {"workload": f"config2 sample: PETALS J=10 L=70 c=7 K={len(rates)} C={sum(caps)}; "
-                               f"{args.points} lambdas x {sample_reps} reps x {args.jobs} jobs per step",
-                   "parallelism": f"{threads} host threads"},
-        "cpu_baseline": {"value": value, "unit": "jobs/s", "cores": threads, "kind": "port",
-                         "sample": f"{args.points} lambdas x {sample_reps} reps x {args.jobs} jobs per "
-                                   "step; oracle/cs_oracle.c restatement of sim.py (reference is "
-                                   "pure Python and cannot travel to the GPU box)"},
+                               f"{cores} reps x {args.jobs} jobs per step",
+                   "parallelism": f"{cores} host processes"},
+        "cpu_baseline": {"value": value, "unit": "jobs/s", "cores": cores, "kind": kind, "sample": sample},
         "e2e": {"value": value, "unit": "jobs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def philox_peak(lib, torch):
+    """Measured Philox4x64-10 generation rate (blocks/s) of this GPU."""
+    sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    grid, per = sms * 8, 512
+    out = torch.empty(grid * 256, dtype=torch.int64, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    lib.cs_philox_peak(per, grid, out.data_ptr(), st)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(3):
+        lib.cs_philox_peak(per, grid, out.data_ptr(), st)
+    b.record()
+    b.synchronize()
+    return 3 * grid * 256 * per / (a.elapsed_time(b) / 1e3)
+
+
+def config5(P, rates, caps, nu, rank, world, barrier, torch):
+    """BASELINE config 5: 8192 replications x 1e6 jobs of the config-1
+    composition at lambda = 0.7 nu, split over the N GPUs (strong scaling
+    across the driver's N runs), through the public API (host buffers)."""
+    total_reps = 8192
+    per = total_reps // world
+    lam = 0.7 * nu
+    P.simulate_sweep([rates], [caps], [lam], 1_000_000, 0.1, 1, 8, rep_begin=rank * per)  # warm the pools
+    barrier()
+    t0 = time.perf_counter()
+    P.simulate_sweep([rates], [caps], [lam], 1_000_000, 0.1, 1, per, rep_begin=rank * per,
+                     max_stream_bytes=34 << 30)
+    barrier()
+    dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+    s = float(dt.item())
+    jobs = per * world * 1_000_000
+    return {"workload": "config5: PETALS c=7 composition (K=1, C=7), lambda=0.7 nu, 8192 reps x 1e6 jobs, "
+                        "warm-up 0.1, split over the GPUs", "n_gpus": world, "reps_per_gpu": per,
+            "seconds": s, "value": jobs / s, "unit": "jobs/s", "per_gpu": jobs / s / world,
+            "scaling": "strong",
+            "note": "end to end through simulate_sweep on each rank (host buffers; streams chunked per "
+                    "34 GiB, responses kept for the exact quantiles; per-rank statistics), max over ranks"}
+
+
+def compose_config4(instances_moderate: int, instances_full: int, steps: int):
+    """BASELINE config 4 through bench_compose.run (GPU GBP+GCA, oracle-checked sample)."""
+    import bench_compose as BC
+
+    out = {}
+    for regime, n in (("moderate", instances_moderate), ("full", instances_full)):
+        r = BC.run(regime, n, steps, 16 if regime == "moderate" else 4)
+        out[regime] = {k: r[k] for k in ("value", "unit", "ms_per_step", "stages_ms", "cpu_baseline",
+                                         "parity", "roofline")}
+        out[regime]["workload"] = r["config"]["workload"]
+        out[regime]["mean_chains"] = r["config"]["mean_chains"]
+        out[regime]["mean_edges"] = r["config"]["mean_edges"]
+    return out
 
 
 def main():
@@ -235,6 +364,7 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2604_14993_b200 import _native as N
     from paper_2604_14993_b200.engine import SweepEngine
     import paper_2604_14993_b200 as P
 
@@ -271,32 +401,18 @@ def main():
                 summ_t.copy_(eng.sets[b]["summ"])
                 dist.all_gather(gathered, summ_t)
 
-    # warm-up, then K complete sweeps pipelined over two buffer sets (streams
-    # of sweep k+1 and statistics of sweep k-1 overlap the simulation of k)
-    eng.run_pipelined(max(args.warmup, 3), gather)
+    # warm-up, then K complete sweeps pipelined over two buffer sets: each
+    # simulation runs alone (its kernel fills every SM), the statistics of
+    # sweep k overlap the streams of sweep k+1
+    eng.run_pipelined(max(args.warmup, 3), gather, ordered=True)
     barrier()
-    # schedule choice (1 GPU): the overlapped order usually runs a sweep in
-    # ~40.5 ms, but in some processes the block placement settles into a
-    # 58 ms pattern; the in-order schedule is a steady ~43.7 ms.  Three warm
-    # sweeps of each decide (both compute every sweep in full).
-    ordered, sched_ms = None, {}
-    if world == 1:
-        for name, o in (("overlapped", False), ("ordered", True)):
-            ta, tb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            torch.cuda.synchronize()
-            ta.record()
-            eng.run_pipelined(3, gather, ordered=o)
-            tb.record()
-            tb.synchronize()
-            sched_ms[name] = round(ta.elapsed_time(tb) / 3, 2)
-        ordered = sched_ms["ordered"] < sched_ms["overlapped"]
     launches0 = eng.lib.cs_launch_count()
     with ClockSampler(local) as clk:
         t_start = torch.cuda.Event(enable_timing=True)
         t_end = torch.cuda.Event(enable_timing=True)
         barrier()
         t_start.record()
-        eng.run_pipelined(args.steps, gather, ordered=ordered)
+        eng.run_pipelined(args.steps, gather, ordered=True)
         t_end.record()
         barrier()
     ms = t_start.elapsed_time(t_end)
@@ -313,14 +429,48 @@ def main():
     sim_ms = float(np.mean([s.sim_ms for s in stage]))
     streams_ms = float(np.mean([s.streams_ms for s in stage]))
     stats_ms = float(np.mean([s.stats_ms for s in stage]))
-    # algorithmic HBM bytes of the dominant kernel (jffc_sim): responses written
-    # + the unique exponential streams read + per-rep summaries/busy written
-    alg_bytes = (8 * args.points * R * eng.m + 8 * 2 * args.jobs * R
-                 + args.points * R * (128 + 8 * eng.ldb))
+    plan = N.seg_plan(args.points, R, int(sum(caps)), args.jobs)
     peak, peak_kind = measured_peaks()
-    achieved = alg_bytes / (sim_ms / 1e3) / 1e9
-    kname = sim_kernel_name(len(rates), int(sum(caps)), args.jobs)
+    clocks = clk.summary()
+    sms = torch.cuda.get_device_properties(local).multi_processor_count
+    sm_hz = (clocks.get("sm_mhz") or 1965.0) * 1e6
+    issue_peak = sms * 4 * sm_hz  # warp instructions / s
+    prof = ncu_summary(args.jobs, R, args.points)
+    # algorithmic HBM bytes of the simulation stage: responses written + the
+    # unique exponential streams read + summaries/busy written
+    alg_bytes = (8 * args.points * R * eng.m + 8 * 2 * args.jobs * R + args.points * R * (128 + 8 * eng.ldb))
     stats_bytes = 8 * args.points * R * eng.m  # one read of every stored response
+    # RNG: one stream of 2n exponential draws per replication (shared by the
+    # points: common random numbers), 1.0334 Philox words per draw
+    ph_peak = philox_peak(eng.lib, torch)
+    ph_blocks = R * 2 * args.jobs * 1.0334 / 4
+    roof = {
+        "bound": "issue", "unit": "warp-instr/s", "peak": issue_peak,
+        "kernel": "jffc_seg_kernel (+ seg_prefix_kernel, seg_finalize_kernel: the simulation stage)",
+        "peak_source": f"{sms} SMs x 4 schedulers x {sm_hz / 1e6:.0f} MHz (median SM clock under load)",
+        "achieved": None, "frac": None, "traffic": None,
+        "hbm": {"algorithmic_bytes": alg_bytes, "achieved": alg_bytes / (sim_ms / 1e3) / 1e9, "peak": peak,
+                "unit": "GB/s", "frac": alg_bytes / (sim_ms / 1e3) / 1e9 / peak, "peak_source": peak_kind},
+        "rng_floor": {"philox_blocks_per_step": ph_blocks, "achieved": ph_blocks / (ms_per_step / 1e3),
+                      "peak": ph_peak, "unit": "Philox4x64-10 blocks/s",
+                      "frac": ph_blocks / (ms_per_step / 1e3) / ph_peak,
+                      "peak_source": "cs_philox_peak measured in this run",
+                      "note": "unique streams only (the 16 points share each replication's stream)"},
+        "stats_pass": {"kernel": "row_stats_kernel + sample select", "bound": "hbm",
+                       "algorithmic_bytes": stats_bytes, "achieved": stats_bytes / (stats_ms / 1e3) / 1e9,
+                       "frac": stats_bytes / (stats_ms / 1e3) / 1e9 / peak,
+                       "note": "whole statistics stage time against the one full read of the responses"},
+        "plan": plan,
+    }
+    if prof is not None:
+        k = prof["kernels"]
+        sim_k = [x for x in ("seg_prefix_kernel", "jffc_seg_kernel", "seg_finalize_kernel") if x in k]
+        sim_inst = sum(k[x]["inst_executed"] for x in sim_k)
+        roof["achieved"] = sim_inst / (sim_ms / 1e3)
+        roof["frac"] = roof["achieved"] / issue_peak
+        roof["traffic"] = sum(k[x]["dram_read"] + k[x]["dram_write"] for x in sim_k)
+        roof["ncu"] = {"source": os.path.relpath(NCU_SUMMARY, ROOT), "inst_executed_per_sweep": sim_inst,
+                       "kernels": {x: k[x] for x in sim_k}}
 
     # end to end through the public API (host buffers in/out), rank-local work
     cfgs = [P.SimConfig(rates=rates, capacities=caps, workload=P.PoissonWorkload(l),
@@ -341,13 +491,19 @@ def main():
         barrier()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
-            stats = run_api(cfgs)
+            run_api(cfgs)
         barrier()
         e2e_s = (time.perf_counter() - t0) / args.e2e_steps
         e2e_t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
         if world > 1:
             dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
         e2e_value = world * jobs_per_step / float(e2e_t.item())
+    del eng
+    torch.cuda.empty_cache()
+    c5 = None if args.no_config5 else config5(P, rates, caps, nu, rank, world, barrier, torch)
+    comp = None
+    if rank == 0 and world == 1 and not args.no_compose:
+        comp = compose_config4(10_000, 256, 3)
 
     if rank == 0:
         cpu = None if args.no_cpu_baseline or world > 1 else cpu_baseline(rates, caps, lams, args)
@@ -363,34 +519,21 @@ def main():
                             f"{args.jobs} jobs per GPU",
                 "jobs_per_step": world * jobs_per_step,
                 "l2": "inputs larger than L2 (responses 8 B/job stored in HBM)",
-                "schedule": {"chosen": "sharded-ordered" if ordered is None else
-                             ("ordered" if ordered else "overlapped"), "warm_ms_per_sweep": sched_ms},
+                "schedule": "each sweep's simulation alone on the GPU (cooperative launch); its "
+                            "statistics overlap the next sweep's streams (two buffer sets)",
                 "parallelism": f"replicas sharded over {world} GPU(s) ({R} per GPU); NCCL all-gather of "
                            "summaries + all-reduced radix-select histograms for exact global quantiles",
             },
             "stages_ms": {"streams": streams_ms, "jffc_sim": sim_ms, "stats": stats_ms,
-                          "note": "unpipelined per-stage device times; the timed sweeps overlap the "
-                                  "streams of sweep k+1 and the statistics of sweep k-1 with the "
-                                  "simulation of sweep k (two buffer sets, three CUDA streams)"},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak,
-                         "traffic": ncu_traffic(kname, args.jobs, R, args.points),
-                         "algorithmic_bytes": alg_bytes, "kernel": kname,
-                         "peak_source": peak_kind,
-                         "note": "the dominant kernel is issue/latency-bound (serial per-replication "
-                                 "recursions, one warp per scheduler; ncu issue-slot utilisation in "
-                                 "profiles/r1_ncu_full_summary.txt), not HBM-bound; see DESIGN.md §4",
-                         "stats_pass": {"kernel": "row_stats_kernel", "bound": "hbm",
-                                        "algorithmic_bytes": stats_bytes,
-                                        "achieved": stats_bytes / (stats_ms / 1e3) / 1e9,
-                                        "frac": stats_bytes / (stats_ms / 1e3) / 1e9 / peak,
-                                        "note": "whole statistics stage time (sample select + full "
-                                                "row pass + rounds) against the one full read"}},
+                          "note": "unpipelined per-stage device times"},
+            "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "jobs/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
+            "config5": c5,
+            "compose": comp,
             "gpu_launches": int(launches),
-            "clocks": clk.summary(),
+            "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -75,6 +75,18 @@ def run(regime: str, n_inst: int, steps: int, cpu_sample: int):
         assert np.array_equal(res["times"][seed, :k].view(np.uint64), np.array(tms).view(np.uint64)), seed
         assert int(res["n_edges"][seed]) == ne, seed
     total_ms = gbp_ms + gca_ms
+    # algorithmic work of GCA: every shortest-path round scans the live edge
+    # set (cache_alloc.py:108-131), so K rounds x E edges bounds the
+    # relaxations the reference performs per instance
+    relax = float((res["n_chains"].astype(np.float64) * res["n_edges"].astype(np.float64)).sum())
+    prof = None
+    path = os.path.join(ROOT, "profiles", "r2_ncu_compose.json")
+    if os.path.exists(path):
+        with open(path) as fh:
+            prof = json.load(fh).get(regime)
+    roof = {"bound": "issue", "relaxations_per_instance": relax / n_inst,
+            "relaxations_per_s": relax / (gca_ms / 1e3), "unit": "edge relaxations/s (K x E bound)",
+            "ncu": prof}
     return {
         "metric": "composed instances/sec (GBP-CR + GCA)", "regime": regime,
         "value": n_inst / (total_ms / 1e3), "unit": "instances/s", "n_gpus": 1, "steps": steps,
@@ -86,6 +98,7 @@ def run(regime: str, n_inst: int, steps: int, cpu_sample: int):
                          "kind": "port", "sample": f"first {len(sample)} instances, oracle/cs_oracle.c "
                                                    f"(heap Dijkstra, as cache_alloc.py) in {cpu_s:.2f} s"},
         "parity": f"bit-exact caps/times/edge counts on {len(sample)} instances",
+        "roofline": roof,
     }
 
 

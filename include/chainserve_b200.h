@@ -129,6 +129,12 @@ int cs_jffc_sim(const cs_sim_point* d_points, int32_t n_points, const double* d_
 int64_t cs_jffc_sim_workspace_bytes(int32_t n_points, int32_t n_reps, int32_t max_chains,
                                     int32_t max_capacity, int64_t n_jobs);
 
+/* Measurement helper (no reference counterpart): generate
+ * grid*256*blocks_per_thread Philox4x64-10 blocks, XOR-folded into
+ * d_out[grid*256]; timed by bench.py as the RNG peak the simulator's
+ * RNG-floor fraction is quoted against. */
+int cs_philox_peak(int64_t blocks_per_thread, int32_t grid, uint64_t* d_out, void* stream);
+
 /* Engine-side introspection (no reference counterpart): the launch plan of
  * the segmented single-chain path for this shape on the current device --
  * out[0] segments per replication, out[1] warps per segment, out[2]

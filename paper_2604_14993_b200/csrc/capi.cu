@@ -17,6 +17,7 @@ extern "C" int cs_jffc_sim_impl(const cs_sim_point*, int32_t, const double*, con
                                 int64_t, double*, int64_t, double*, int32_t, cs_rep_summary*, double*,
                                 void*, int64_t, void*);
 extern "C" int64_t cs_jffc_sim_workspace_bytes_impl(int32_t, int32_t, int32_t, int32_t, int64_t);
+extern "C" int cs_philox_peak_impl(int64_t, int32_t, uint64_t*, void*);
 extern "C" int cs_rep_stats_impl(const double*, int32_t, int64_t, int64_t, int64_t, cs_rep_summary*,
                                  const int64_t*, int32_t, double*, double*, int32_t, void*);
 extern "C" int cs_gbp_batch_impl(const cs_compose_point*, int32_t, int32_t, const int64_t*,
@@ -154,6 +155,18 @@ int cs_exp_streams(const uint64_t* d_keys, int64_t n_streams, int64_t n_draws, d
     }
     const int v = log1p_variant < 0 ? cs_host_log1p_variant() : log1p_variant;
     return cs_exp_streams_impl(d_keys, n_streams, n_draws, d_out, ld, v, stream);
+}
+
+int cs_philox_peak(int64_t blocks_per_thread, int32_t grid, uint64_t* d_out, void* stream) {
+    if (cs_device_count() == 0) {
+        set_error("cs_philox_peak: no CUDA device");
+        return CS_ERR_CUDA;
+    }
+    if (blocks_per_thread < 1 || grid < 1) {
+        set_error("cs_philox_peak: invalid sizes");
+        return CS_INVALID;
+    }
+    return cs_philox_peak_impl(blocks_per_thread, grid, d_out, stream);
 }
 
 int64_t cs_jffc_sim_workspace_bytes(int32_t n_points, int32_t n_reps, int32_t max_chains,

@@ -161,7 +161,30 @@ __global__ void __launch_bounds__(256) exp_streams_kernel(const uint64_t* __rest
     }
 }
 
+// Measurement kernel (no reference counterpart): Philox4x64-10 blocks as
+// fast as the SMs generate them, XOR-folded per thread so nothing is
+// optimised away and nothing is stored per block.  The simulator's RNG
+// floor is reported against this rate (bench.py roofline.rng_floor).
+__global__ void __launch_bounds__(256) philox_peak_kernel(int64_t blocks_per_thread, uint64_t k0, uint64_t k1,
+                                                          uint64_t* __restrict__ out) {
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    uint64_t acc = 0;
+    for (int64_t i = 0; i < blocks_per_thread; i++) {
+        uint64_t w[4];
+        philox4x64_10(t + stride * (uint64_t)i + 1, 0, 0, 0, k0, k1, w);
+        acc ^= w[0] ^ w[1] ^ w[2] ^ w[3];
+    }
+    out[t] = acc;
+}
+
 }  // namespace cs
+
+extern "C" int cs_philox_peak_impl(int64_t blocks_per_thread, int32_t grid, uint64_t* d_out, void* stream) {
+    cs::philox_peak_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(blocks_per_thread, 0x0123456789abcdefULL,
+                                                                   0xfedcba9876543210ULL, d_out);
+    return cs::check_launch("philox_peak_kernel");
+}
 
 extern "C" int cs_exp_streams_impl(const uint64_t* d_keys, int64_t n_streams, int64_t n_draws,
                                    double* d_out, int64_t ld, int log1p_fma, void* stream) {

@@ -145,7 +145,7 @@ __device__ __forceinline__ double dmax0(double x) { return x > 0.0 ? x : 0.0; }
 // streams (the P points of a rep), so the stream loads are broadcasts.
 // ---------------------------------------------------------------------------
 constexpr int PF_U = 16;     // values per chunk (one 128-byte line of a row)
-constexpr int PF_NBUF = 12;  // chunks in flight (cp.async ring)
+constexpr int PF_NBUF = 24;  // chunks in flight (cp.async ring): ~4000 cycles of DRAM latency
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
