@@ -129,6 +129,28 @@ int cs_jffc_sim(const cs_sim_point* d_points, int32_t n_points, const double* d_
 int64_t cs_jffc_sim_workspace_bytes(int32_t n_points, int32_t n_reps, int32_t max_chains,
                                     int32_t max_capacity, int64_t n_jobs);
 
+/* cs_exp_streams for a following cs_jffc_sim_ex of the same shape: when the
+ * segmented single-chain path applies (and n_points <= 32), the stream kernel
+ * also runs the exact arrival-time cumsum of every (replication, point) row
+ * and records the simulator's per-segment start times into d_workspace
+ * (sized by cs_jffc_sim_workspace_bytes); *prefix_ready is then 1 and the
+ * simulation call takes flags CS_SIM_PREFIX_READY (it skips its own pre-pass). */
+#define CS_SIM_PREFIX_READY 1
+int cs_sim_streams(const uint64_t* d_keys, int64_t n_streams, int64_t n_draws, double* d_out, int64_t ld,
+                   int32_t log1p_variant, const cs_sim_point* d_points, int32_t n_points,
+                   int32_t max_chains, int32_t max_capacity, int64_t n_jobs, int64_t warm,
+                   void* d_workspace, int64_t workspace_bytes, int32_t* prefix_ready, void* stream);
+
+/* cs_jffc_sim with flags (CS_SIM_PREFIX_READY: d_workspace holds the prefix
+ * cs_sim_streams wrote for exactly these streams and shape). */
+int cs_jffc_sim_ex(const cs_sim_point* d_points, int32_t n_points, const double* d_rates,
+                   const int32_t* d_caps, int32_t max_chains, int32_t max_capacity,
+                   const double* d_streams, int64_t lds, int32_t rep_begin, int32_t n_reps,
+                   int32_t n_reps_total, int64_t n_jobs, int64_t warm, double* d_responses,
+                   int64_t ldr, double* d_busy, int32_t ldb, cs_rep_summary* d_summary,
+                   double* d_jobs, void* d_workspace, int64_t workspace_bytes, int32_t flags,
+                   void* stream);
+
 /* Measurement helper (no reference counterpart): generate
  * grid*256*blocks_per_thread Philox4x64-10 blocks, XOR-folded into
  * d_out[grid*256]; timed by bench.py as the RNG peak the simulator's

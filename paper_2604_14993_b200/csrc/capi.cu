@@ -15,7 +15,14 @@ extern "C" int cs_exp_streams_impl(const uint64_t*, int64_t, int64_t, double*, i
 extern "C" int cs_jffc_sim_impl(const cs_sim_point*, int32_t, const double*, const int32_t*, int32_t,
                                 int32_t, const double*, int64_t, int32_t, int32_t, int32_t, int64_t,
                                 int64_t, double*, int64_t, double*, int32_t, cs_rep_summary*, double*,
-                                void*, int64_t, void*);
+                                void*, int64_t, int32_t, void*);
+extern "C" int cs_exp_streams_prefix_impl(const uint64_t*, int64_t, int64_t, double*, int64_t, int,
+                                          const cs::PrefixPlan*, void*);
+extern "C" bool cs_seg_prefix_plan(int32_t, int32_t, int32_t, int64_t, int64_t, const cs_sim_point*, void*,
+                                   cs::PrefixPlan*);
+namespace cs {
+bool use_seg(int32_t max_chains, int32_t max_cap, int64_t n);
+}
 extern "C" int64_t cs_jffc_sim_workspace_bytes_impl(int32_t, int32_t, int32_t, int32_t, int64_t);
 extern "C" int cs_philox_peak_impl(int64_t, int32_t, uint64_t*, void*);
 extern "C" int cs_rep_stats_impl(const double*, int32_t, int64_t, int64_t, int64_t, cs_rep_summary*,
@@ -174,24 +181,62 @@ int64_t cs_jffc_sim_workspace_bytes(int32_t n_points, int32_t n_reps, int32_t ma
     return cs_jffc_sim_workspace_bytes_impl(n_points, n_reps, max_chains, max_capacity, n_jobs);
 }
 
+int cs_jffc_sim_ex(const cs_sim_point* d_points, int32_t n_points, const double* d_rates,
+                   const int32_t* d_caps, int32_t max_chains, int32_t max_capacity,
+                   const double* d_streams, int64_t lds, int32_t rep_begin, int32_t n_reps,
+                   int32_t n_reps_total, int64_t n_jobs, int64_t warm, double* d_responses, int64_t ldr,
+                   double* d_busy, int32_t ldb, cs_rep_summary* d_summary, double* d_jobs,
+                   void* d_workspace, int64_t workspace_bytes, int32_t flags, void* stream) {
+    if (cs_device_count() == 0) {
+        set_error("cs_jffc_sim: no CUDA device");
+        return CS_ERR_CUDA;
+    }
+    if (n_jobs < 1 || warm < 0 || warm >= n_jobs || max_chains < 1 || max_capacity < 1 ||
+        ldb < max_chains || lds < 2 * n_jobs || rep_begin < 0 || rep_begin + n_reps > n_reps_total ||
+        (ldr & 1)) {
+        set_error("cs_jffc_sim: invalid sizes");
+        return CS_INVALID;
+    }
+    return cs_jffc_sim_impl(d_points, n_points, d_rates, d_caps, max_chains, max_capacity, d_streams,
+                            lds, rep_begin, n_reps, n_reps_total, n_jobs, warm, d_responses, ldr,
+                            d_busy, ldb, d_summary, d_jobs, d_workspace, workspace_bytes, flags, stream);
+}
+
 int cs_jffc_sim(const cs_sim_point* d_points, int32_t n_points, const double* d_rates,
                 const int32_t* d_caps, int32_t max_chains, int32_t max_capacity,
                 const double* d_streams, int64_t lds, int32_t rep_begin, int32_t n_reps,
                 int32_t n_reps_total, int64_t n_jobs, int64_t warm, double* d_responses, int64_t ldr,
                 double* d_busy, int32_t ldb, cs_rep_summary* d_summary, double* d_jobs,
                 void* d_workspace, int64_t workspace_bytes, void* stream) {
+    return cs_jffc_sim_ex(d_points, n_points, d_rates, d_caps, max_chains, max_capacity, d_streams, lds,
+                          rep_begin, n_reps, n_reps_total, n_jobs, warm, d_responses, ldr, d_busy, ldb,
+                          d_summary, d_jobs, d_workspace, workspace_bytes, 0, stream);
+}
+
+int cs_sim_streams(const uint64_t* d_keys, int64_t n_streams, int64_t n_draws, double* d_out, int64_t ld,
+                   int32_t log1p_variant, const cs_sim_point* d_points, int32_t n_points,
+                   int32_t max_chains, int32_t max_capacity, int64_t n_jobs, int64_t warm,
+                   void* d_workspace, int64_t workspace_bytes, int32_t* prefix_ready, void* stream) {
+    if (prefix_ready) *prefix_ready = 0;
     if (cs_device_count() == 0) {
-        set_error("cs_jffc_sim: no CUDA device");
+        set_error("cs_sim_streams: no CUDA device");
         return CS_ERR_CUDA;
     }
-    if (n_jobs < 1 || warm < 0 || warm >= n_jobs || max_chains < 1 || max_capacity < 1 ||
-        ldb < max_chains || lds < 2 * n_jobs || rep_begin < 0 || rep_begin + n_reps > n_reps_total) {
-        set_error("cs_jffc_sim: invalid sizes");
+    if (ld < n_draws || n_jobs < 1 || warm < 0 || warm >= n_jobs || n_draws < 2 * n_jobs) {
+        set_error("cs_sim_streams: invalid sizes");
         return CS_INVALID;
     }
-    return cs_jffc_sim_impl(d_points, n_points, d_rates, d_caps, max_chains, max_capacity, d_streams,
-                            lds, rep_begin, n_reps, n_reps_total, n_jobs, warm, d_responses, ldr,
-                            d_busy, ldb, d_summary, d_jobs, d_workspace, workspace_bytes, stream);
+    const int v = log1p_variant < 0 ? cs_host_log1p_variant() : log1p_variant;
+    cs::PrefixPlan pp;
+    const int64_t need = cs_jffc_sim_workspace_bytes_impl(n_points, (int32_t)n_streams, max_chains,
+                                                          max_capacity, n_jobs);
+    if (prefix_ready && d_workspace && workspace_bytes >= need && cs::use_seg(max_chains, max_capacity, n_jobs) &&
+        cs_seg_prefix_plan(n_points, (int32_t)n_streams, max_capacity, n_jobs, warm, d_points, d_workspace, &pp)) {
+        const int rc = cs_exp_streams_prefix_impl(d_keys, n_streams, n_draws, d_out, ld, v, &pp, stream);
+        if (rc == CS_OK) *prefix_ready = 1;
+        return rc;
+    }
+    return cs_exp_streams_impl(d_keys, n_streams, n_draws, d_out, ld, v, stream);
 }
 
 int cs_rep_stats(const double* d_resp, int32_t n_groups, int64_t rows_per_group, int64_t m,
@@ -330,14 +375,17 @@ int cs_run_sim_host(const cs_sim_point* points, int32_t n_points, const double* 
         if ((rc = cs_philox_keys(entropy, n_entropy, reps.data(), cn, keys.data()))) return rc;
         // the host vector is reused next chunk: order the copy before it
         cudaMemcpyAsync(b_keys.p, keys.data(), sizeof(uint64_t) * 2 * cn, cudaMemcpyHostToDevice, st);
-        if ((rc = cs_exp_streams((const uint64_t*)b_keys.p, cn, lds, (double*)b_S.p, lds,
-                                 log1p_variant, st)))
+        int32_t ready = 0;
+        if ((rc = cs_sim_streams((const uint64_t*)b_keys.p, cn, lds, (double*)b_S.p, lds, log1p_variant,
+                                 (const cs_sim_point*)b_pts.p, n_points, max_chains, max_cap, n_jobs, warm,
+                                 out_jobs ? nullptr : b_ws.p, wsb, &ready, st)))
             return rc;
         if ((rc = cs_jffc_sim_impl((const cs_sim_point*)b_pts.p, n_points, (const double*)b_rates.p,
                                    (const int32_t*)b_caps.p, max_chains, max_cap, (const double*)b_S.p,
                                    lds, (int32_t)c0, (int32_t)cn, n_reps, n_jobs, warm,
                                    (double*)b_resp.p, ldr, (double*)b_busy.p, ldb,
-                                   (cs_rep_summary*)b_summ.p, (double*)b_jobs.p, b_ws.p, wsb, st)))
+                                   (cs_rep_summary*)b_summ.p, (double*)b_jobs.p, b_ws.p, wsb,
+                                   ready ? CS_SIM_PREFIX_READY : 0, st)))
             return rc;
         if (c0 + chunk < n_reps && (rc = check_cuda(cudaStreamSynchronize(st), "chunk sync"))) return rc;
     }

@@ -44,6 +44,20 @@ int allreduce_u32(void* buf, size_t count, cudaStream_t st);
 int allreduce_u64(void* buf, size_t count, cudaStream_t st);
 int allreduce_max_u64(void* buf, size_t count, cudaStream_t st);
 
+// Arrival-time prefix of the segmented single-chain simulator, computed
+// while the exponential streams are generated (exp_stream.cu, jffc_seg.cu).
+struct PrefixPlan {
+    static constexpr int MAXEV = 72;   // job indices recorded per row
+    static constexpr int MAXP32 = 1;   // points per stream: up to 32 (more: the standalone pre-pass)
+    const cs_sim_point* pts;           // lam of every point
+    int32_t P;                         // points sharing each stream
+    int32_t nev, ncol;
+    int64_t n_cum;                     // the first n_cum draws are the gaps
+    int32_t ev_idx[MAXEV];             // ascending job indices
+    int32_t ev_col[MAXEV];             // output column of each
+    double* out;                       // [stream * P + p][ncol]
+};
+
 // Python-semantics helpers (no contraction; explicit IEEE round-to-nearest).
 __device__ __forceinline__ double py_div(double a, double b) { return __ddiv_rn(a, b); }
 

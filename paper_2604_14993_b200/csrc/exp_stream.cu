@@ -27,12 +27,20 @@ struct Xfer {
     int c0, c1;  // values emitted for entry 0 / 1
 };
 
+// Fused arrival-time prefix (the segmented simulator's pre-pass, see
+// jffc_seg.cu): while the first n_cum draws of stream r are generated, lane p
+// of its warp (p < P, the sweep points sharing the stream) runs the exact
+// sequential cumsum a_j = a_{j-1} + (1/lam_p) * S_j of np.cumsum and records
+// a_j at the listed job indices into out[(r * P + p) * ncol + col].
+template <bool PFX>
 __global__ void __launch_bounds__(256) exp_streams_kernel(const uint64_t* __restrict__ keys,
                                                           int64_t n_streams, int64_t n_draws,
                                                           double* __restrict__ out, int64_t ld,
                                                           int log1p_fma,
-                                                          int64_t* __restrict__ words_used) {
+                                                          int64_t* __restrict__ words_used,
+                                                          const PrefixPlan pp) {
     __shared__ ZigSmem zs;
+    __shared__ double sh_vals[PFX ? 8 : 1][136];  // a chunk's values (<= 128 + carry), per warp
     zig_load(&zs);
     __syncthreads();
     const int lane = threadIdx.x & 31;
@@ -40,6 +48,19 @@ __global__ void __launch_bounds__(256) exp_streams_kernel(const uint64_t* __rest
     if (stream >= n_streams) return;
     const uint64_t k0 = keys[2 * stream], k1 = keys[2 * stream + 1];
     double* __restrict__ o = out + stream * ld;
+    double* cv = sh_vals[PFX ? (threadIdx.x >> 5) : 0];
+    // prefix state: lane p handles point p (P <= 32 per pass; more points loop)
+    double pa[PFX ? PrefixPlan::MAXP32 : 1];
+    double pscale[PFX ? PrefixPlan::MAXP32 : 1];
+    int ev = 0;  // next event of the (uniform) event list
+    if (PFX) {
+#pragma unroll
+        for (int g = 0; g < PrefixPlan::MAXP32; g++) {
+            const int p = g * 32 + lane;
+            pscale[g] = p < pp.P ? __ddiv_rn(1.0, pp.pts[p].lam) : 0.0;
+            pa[g] = 0.0;
+        }
+    }
 
     int64_t produced = 0;
     int entry = 0;            // warp-uniform: offset of the first attempt in this chunk
@@ -132,6 +153,7 @@ __global__ void __launch_bounds__(256) exp_streams_kernel(const uint64_t* __rest
         int64_t base = produced + pos;
         if (carry_has) {
             if (base < n_draws) o[base] = carry_v;
+            if (PFX) cv[base - produced] = carry_v;
             base++;
         }
         {
@@ -141,6 +163,7 @@ __global__ void __launch_bounds__(256) exp_streams_kernel(const uint64_t* __rest
                 if (p == q) {
                     if (has[q]) {
                         if (base < n_draws) o[base] = v[q];
+                        if (PFX) cv[base - produced] = v[q];
                         base++;
                     }
                     p += adv[q];
@@ -150,6 +173,42 @@ __global__ void __launch_bounds__(256) exp_streams_kernel(const uint64_t* __rest
         const int tot = __shfl_sync(0xffffffffu, entry ? inc.c1 : inc.c0, 31);
         const int nxt = __shfl_sync(0xffffffffu, entry ? inc.x1 : inc.x0, 31);
         pend_w = __shfl_sync(0xffffffffu, w[3], 31);
+        if (PFX && produced < pp.n_cum) {
+            __syncwarp();
+            const int cnt = (int)min((int64_t)tot, pp.n_cum - produced);
+            const int32_t j0 = (int32_t)produced;
+#pragma unroll
+            for (int g = 0; g < PrefixPlan::MAXP32; g++) {
+                const int p = g * 32 + lane;
+                if (g * 32 >= pp.P) break;
+                double a = pa[g];
+                const double sc = pscale[g];
+                int e = ev;
+                if (j0 > 0 && (e >= pp.nev || pp.ev_idx[e] >= j0 + cnt)) {  // no event in the chunk
+                    int i = 0;
+                    for (; i + 4 <= cnt; i += 4) {
+                        a = __dadd_rn(a, __dmul_rn(sc, cv[i]));
+                        a = __dadd_rn(a, __dmul_rn(sc, cv[i + 1]));
+                        a = __dadd_rn(a, __dmul_rn(sc, cv[i + 2]));
+                        a = __dadd_rn(a, __dmul_rn(sc, cv[i + 3]));
+                    }
+                    for (; i < cnt; i++) a = __dadd_rn(a, __dmul_rn(sc, cv[i]));
+                } else {
+                    for (int i = 0; i < cnt; i++) {
+                        const double x = __dmul_rn(sc, cv[i]);
+                        const int32_t j = j0 + i;
+                        a = j == 0 ? x : __dadd_rn(a, x);
+                        while (e < pp.nev && pp.ev_idx[e] == j) {
+                            if (p < pp.P) pp.out[((int64_t)stream * pp.P + p) * pp.ncol + pp.ev_col[e]] = a;
+                            e++;
+                        }
+                    }
+                }
+                pa[g] = a;
+                ev = e;
+            }
+            __syncwarp();
+        }
         produced += tot;
         entry = nxt;
         chunk++;
@@ -191,7 +250,20 @@ extern "C" int cs_exp_streams_impl(const uint64_t* d_keys, int64_t n_streams, in
     if (n_streams <= 0 || n_draws <= 0) return 0;
     const int warps_per_block = 8;
     const int64_t blocks = (n_streams + warps_per_block - 1) / warps_per_block;
-    cs::exp_streams_kernel<<<(unsigned)blocks, warps_per_block * 32, 0, (cudaStream_t)stream>>>(
-        d_keys, n_streams, n_draws, d_out, ld, log1p_fma, nullptr);
+    cs::PrefixPlan none{};
+    cs::exp_streams_kernel<false><<<(unsigned)blocks, warps_per_block * 32, 0, (cudaStream_t)stream>>>(
+        d_keys, n_streams, n_draws, d_out, ld, log1p_fma, nullptr, none);
     return cs::check_launch("exp_streams_kernel");
+}
+
+// Streams plus the segmented simulator's arrival-time prefix (jffc_seg.cu).
+extern "C" int cs_exp_streams_prefix_impl(const uint64_t* d_keys, int64_t n_streams, int64_t n_draws,
+                                          double* d_out, int64_t ld, int log1p_fma,
+                                          const cs::PrefixPlan* plan, void* stream) {
+    if (n_streams <= 0 || n_draws <= 0) return 0;
+    const int warps_per_block = 8;
+    const int64_t blocks = (n_streams + warps_per_block - 1) / warps_per_block;
+    cs::exp_streams_kernel<true><<<(unsigned)blocks, warps_per_block * 32, 0, (cudaStream_t)stream>>>(
+        d_keys, n_streams, n_draws, d_out, ld, log1p_fma, nullptr, *plan);
+    return cs::check_launch("exp_streams_kernel<prefix>");
 }

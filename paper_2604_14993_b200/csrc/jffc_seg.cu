@@ -791,6 +791,36 @@ extern "C" int64_t cs_seg_workspace_bytes_impl(int32_t P, int32_t R, int32_t max
     return (int64_t)cs::seg::make_plan(P, R, max_cap, n).bytes;
 }
 
+// The arrival-time prefix plan for the fused stream kernel (exp_stream.cu):
+// rows of the workspace's prefix table, recorded at the segment starts and
+// the warm-up / mid / last arrivals.  Returns false when the fused path does
+// not apply (more than 32 points per stream or more events than the plan holds).
+extern "C" bool cs_seg_prefix_plan(int32_t P, int32_t R, int32_t max_cap, int64_t n, int64_t warm,
+                                   const cs_sim_point* d_points, void* d_ws, cs::PrefixPlan* pp) {
+    using namespace cs::seg;
+    const Plan pl = make_plan(P, R, max_cap, n);
+    if (P > 32 * cs::PrefixPlan::MAXP32 || pl.S + 3 > cs::PrefixPlan::MAXEV) return false;
+    const int S = pl.S;
+    const int64_t mid = warm + (n - warm) / 2;
+    std::vector<std::pair<int64_t, int>> ev;
+    for (int s = 0; s < S; s++) ev.push_back({seg_begin(s, S, n), s});
+    ev.push_back({warm, S});
+    ev.push_back({mid, S + 1});
+    ev.push_back({n - 1, S + 2});
+    std::stable_sort(ev.begin(), ev.end(), [](auto& a, auto& b) { return a.first < b.first; });
+    pp->pts = d_points;
+    pp->P = P;
+    pp->nev = (int32_t)ev.size();
+    pp->ncol = S + 3;
+    pp->n_cum = n;
+    for (size_t i = 0; i < ev.size(); i++) {
+        pp->ev_idx[i] = (int32_t)ev[i].first;
+        pp->ev_col[i] = ev[i].second;
+    }
+    pp->out = (double*)((char*)d_ws + pl.off_prefix);
+    return true;
+}
+
 // The plan the segmented path would use: out[0..4) = segments per row,
 // warps per segment, checkpoints per segment, slot capacity instance.
 extern "C" int cs_seg_plan(int32_t P, int32_t R, int32_t max_cap, int64_t n, int32_t* out) {
@@ -809,7 +839,8 @@ extern "C" int cs_seg_sim_impl(const cs_sim_point* d_points, int32_t P, const do
                                const int32_t* d_caps, int32_t max_cap, const double* d_streams,
                                int64_t lds, int32_t rb, int32_t R, int32_t RT, int64_t n, int64_t warm,
                                double* d_resp, int64_t ldr, double* d_busy, int32_t ldb,
-                               cs_rep_summary* d_summ, void* d_ws, int64_t ws_bytes, void* stream) {
+                               cs_rep_summary* d_summ, void* d_ws, int64_t ws_bytes, int prefix_ready,
+                               void* stream) {
     using namespace cs;
     using namespace cs::seg;
     const Plan pl = make_plan(P, R, max_cap, n);
@@ -854,20 +885,20 @@ extern "C" int cs_seg_sim_impl(const cs_sim_point* d_points, int32_t P, const do
                         "seg workspace reset");
     if (rc) return rc;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-    if (getenv("CS_SEG_TRACE")) {
+    if (!prefix_ready && getenv("CS_SEG_TRACE")) {
         cudaEventCreate(&ev0);
         cudaEventCreate(&ev1);
         cudaEventRecord(ev0, st);
     }
-    {
+    if (!prefix_ready) {
         // ring of the prefix pass: PF_NBUF chunks x (distinct rows per warp) lines
         const int rows_per_warp = (int)std::min<int64_t>(32, (31 + P - 1) / P + 1);
         const size_t smem = sizeof(double) * PF_NBUF * rows_per_warp * PF_U;
         if (smem > 48 * 1024)
             cudaFuncSetAttribute(seg_prefix_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         seg_prefix_kernel<<<(int)((pl.T + 31) / 32), 32, smem, st>>>(A);
+        if ((rc = check_launch("seg_prefix_kernel"))) return rc;
     }
-    if ((rc = check_launch("seg_prefix_kernel"))) return rc;
     if (ev0) {
         cudaEventRecord(ev1, st);
         cudaEventSynchronize(ev1);

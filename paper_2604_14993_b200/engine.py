@@ -76,13 +76,13 @@ class SweepEngine:
                                         reps, N.ptr(keys, C.c_uint64)), "cs_philox_keys")
         self.h_keys = keys
         self.d_keys = torch.from_numpy(keys.view(np.int64)).to(dev)
+        # simulator workspace per buffer set (the segmented path's prefix is
+        # written by the streams stage of the same set)
+        self.ws_bytes = self.lib.cs_jffc_sim_workspace_bytes(self.P, reps, self.max_chains, self.max_cap, n_jobs)
         # buffer sets: one for step(), a second one for the pipelined sweep
         self.sets = [self._alloc_set()]
         self.d_S, self.d_resp = self.sets[0]["S"], self.sets[0]["resp"]
         self.d_busy, self.d_summ = self.sets[0]["busy"], self.sets[0]["summ"]
-        wsb = self.lib.cs_jffc_sim_workspace_bytes(self.P, reps, self.max_chains, self.max_cap, n_jobs)
-        self.d_ws = torch.empty(max(wsb, 16), dtype=torch.uint8, device=dev)
-        self.ws_bytes = wsb
         # sharded (distributed=True): ranks index the union of all shards' responses
         self.distributed = distributed
         N_total = (total_reps if distributed and total_reps else reps) * self.m
@@ -98,25 +98,30 @@ class SweepEngine:
                 "resp": torch.empty(self.P * self.R * self.ldr, dtype=f64, device=dev),
                 "busy": torch.empty(self.P * self.R * self.ldb, dtype=f64, device=dev),
                 "summ": torch.empty(self.P * self.R * C.sizeof(N.RepSummary), dtype=torch.uint8,
-                                    device=dev)}
+                                    device=dev),
+                "ws": torch.empty(max(self.ws_bytes, 16), dtype=torch.uint8, device=dev),
+                "ready": C.c_int32(0)}
 
     # -- stages (buffer set b, CUDA stream st) ------------------------------
     def streams(self, b: int = 0, st=None):
         st = st or self.stream
-        S = self.sets[b]["S"]
-        rc = self.lib.cs_exp_streams(self.d_keys.data_ptr(), self.R, self.lds, S.data_ptr(), self.lds,
-                                     self.log1p_variant, st.cuda_stream)
-        N.check(rc, "cs_exp_streams")
+        B = self.sets[b]
+        rc = self.lib.cs_sim_streams(self.d_keys.data_ptr(), self.R, self.lds, B["S"].data_ptr(), self.lds,
+                                     self.log1p_variant, self.d_pts.data_ptr(), self.P, self.max_chains,
+                                     self.max_cap, self.n, self.warm, B["ws"].data_ptr(), self.ws_bytes,
+                                     C.byref(B["ready"]), st.cuda_stream)
+        N.check(rc, "cs_sim_streams")
 
     def simulate(self, b: int = 0, st=None):
         st = st or self.stream
         B = self.sets[b]
-        rc = self.lib.cs_jffc_sim(
+        rc = self.lib.cs_jffc_sim_ex(
             self.d_pts.data_ptr(), self.P, self.d_rates.data_ptr(), self.d_caps.data_ptr(),
             self.max_chains, self.max_cap, B["S"].data_ptr(), self.lds, 0, self.R, self.R, self.n,
             self.warm, B["resp"].data_ptr(), self.ldr, B["busy"].data_ptr(), self.ldb,
-            B["summ"].data_ptr(), None, self.d_ws.data_ptr(), self.ws_bytes, st.cuda_stream)
-        N.check(rc, "cs_jffc_sim")
+            B["summ"].data_ptr(), None, B["ws"].data_ptr(), self.ws_bytes,
+            N.CS_SIM_PREFIX_READY if B["ready"].value else 0, st.cuda_stream)
+        N.check(rc, "cs_jffc_sim_ex")
 
     def statistics(self, b: int = 0, st=None):
         st = st or self.stream

@@ -120,3 +120,35 @@ def test_long_rows_vs_oracle(eng, oracle):
     res = eng.simulate_sweep([system.rates], [system.capacities], [lam], n, 0.1, 1, R,
                              return_responses=True)
     _check_rows(res, 0, oracle, system.rates, system.capacities, lam, n, 0.1, 1, R)
+
+
+def test_many_points_standalone_prefix(eng, oracle):
+    """40 points share each stream (> 32: the stream kernel does not fuse the
+    arrival-time prefix, the simulator's own pre-pass computes it)."""
+    rates, caps = (0.8,), (4,)
+    lams = [x * 0.8 * 4 for x in np.linspace(0.1, 0.98, 40)]
+    n, R = 9_000, 3
+    res = eng.simulate_sweep([rates] * 40, [caps] * 40, lams, n, 0.1, 5, R, return_responses=True)
+    for p in (0, 21, 39):
+        _check_rows(res, p, oracle, rates, caps, lams[p], n, 0.1, 5, R)
+
+
+def test_engine_fused_prefix_equals_host_path(eng):
+    """SweepEngine (streams stage writes the simulator's prefix into its
+    buffer set's workspace) equals the host-buffer path bit for bit."""
+    import torch
+
+    from paper_2604_14993_b200.engine import SweepEngine
+
+    system = _petals(eng)
+    lams = [system.total_rate * x for x in (0.2, 0.6, 0.9)]
+    n, R = 30_000, 40
+    e = SweepEngine([system.rates] * 3, [system.capacities] * 3, lams, n, 0.1, 2, R)
+    e.step()
+    torch.cuda.synchronize()
+    assert e.sets[0]["ready"].value == 1
+    res = eng.simulate_sweep([system.rates] * 3, [system.capacities] * 3, lams, n, 0.1, 2, R)
+    got = e.summaries(0)
+    for f in ("wait_sum", "service_sum", "mean_occupancy", "end_queue_len", "window_s", "resp_mean"):
+        assert np.array_equal(np.asarray(got[f]).view(np.uint64), np.asarray(res.summaries[f]).view(np.uint64)), f
+    assert e.order_stats() == res.order_stats
