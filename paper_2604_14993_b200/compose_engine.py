@@ -122,4 +122,6 @@ class ComposeEngine:
                     n_chains=h(self.c_nch), n_edges=h(self.c_ne),
                     caps=h(self.c_caps).reshape(self.P, self.max_chains),
                     times=h(self.c_times).reshape(self.P, self.max_chains),
-                    first=h(self.first).reshape(self.P, self.J), count=h(self.count).reshape(self.P, self.J))
+                    first=h(self.first).reshape(self.P, self.J), count=h(self.count).reshape(self.P, self.J),
+                    chain_len=h(self.c_len).reshape(self.P, self.max_chains),
+                    chain_srv=h(self.c_srv).reshape(self.P, self.max_chains, self.max_hops))
