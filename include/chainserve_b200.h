@@ -136,6 +136,10 @@ int64_t cs_jffc_sim_workspace_bytes(int32_t n_points, int32_t n_reps, int32_t ma
  * (sized by cs_jffc_sim_workspace_bytes); *prefix_ready is then 1 and the
  * simulation call takes flags CS_SIM_PREFIX_READY (it skips its own pre-pass). */
 #define CS_SIM_PREFIX_READY 1
+/* cs_jffc_sim_ex: take the per-event register kernel for single-chain
+ * compositions instead of the serial recursion kernel (its fallback when
+ * exact finish-time ties back up the recursion's merge feed: counted = -1) */
+#define CS_SIM_FORCE_EVENT_LOOP 2
 int cs_sim_streams(const uint64_t* d_keys, int64_t n_streams, int64_t n_draws, double* d_out, int64_t ld,
                    int32_t log1p_variant, const cs_sim_point* d_points, int32_t n_points,
                    int32_t max_chains, int32_t max_capacity, int64_t n_jobs, int64_t warm,

@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <mutex>
 #include <vector>
 
 #include "cs_internal.cuh"
@@ -49,17 +50,40 @@ void set_error(const char* fmt, ...) {
 static std::atomic<long long> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
-void ensure_mem_pool() {
-    static thread_local int done_dev = -1;
+// The engine's own stream-ordered pool per device (not the device's default
+// pool, which other libraries share): up to 4 GiB of freed scratch stays
+// reserved across calls (the statistics' small per-call buffers), anything
+// beyond is returned to the driver at the next synchronisation (the
+// multi-GB response / stream buffers of cs_run_sim_host).
+static cudaMemPool_t g_pools[64] = {};
+
+void ensure_mem_pool() { (void)engine_pool(); }
+
+cudaMemPool_t engine_pool() {
     int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess) return;
-    if (dev == done_dev) return;
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        uint64_t thr = UINT64_MAX;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    if (cudaGetDevice(&dev) != cudaSuccess || dev >= 64) return nullptr;
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lk(mu);
+    if (!g_pools[dev]) {
+        cudaMemPoolProps props = {};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        if (cudaMemPoolCreate(&g_pools[dev], &props) != cudaSuccess) {
+            cudaGetLastError();
+            g_pools[dev] = nullptr;
+            return nullptr;
+        }
+        uint64_t thr = 4ull << 30;
+        cudaMemPoolSetAttribute(g_pools[dev], cudaMemPoolAttrReleaseThreshold, &thr);
     }
-    done_dev = dev;
+    return g_pools[dev];
+}
+
+int pool_alloc(void** p, size_t n, cudaStream_t st) {
+    cudaMemPool_t pool = engine_pool();
+    const cudaError_t e = pool ? cudaMallocFromPoolAsync(p, n ? n : 16, pool, st) : cudaMallocAsync(p, n ? n : 16, st);
+    return check_cuda(e, "cudaMallocFromPoolAsync");
 }
 
 // ---- numpy SeedSequence (bit_generator.pyx), restated for the product ----
@@ -310,7 +334,7 @@ struct DevBuf {
     int alloc(size_t n, cudaStream_t s) {
         st = s;
         if (n == 0) n = 16;
-        return check_cuda(cudaMallocAsync(&p, n, s), "cudaMallocAsync");
+        return pool_alloc(&p, n, s);
     }
 };
 
@@ -387,6 +411,25 @@ int cs_run_sim_host(const cs_sim_point* points, int32_t n_points, const double* 
                                    (cs_rep_summary*)b_summ.p, (double*)b_jobs.p, b_ws.p, wsb,
                                    ready ? CS_SIM_PREFIX_READY : 0, st)))
             return rc;
+        // the serial single-chain kernel (exact mode / job records) flags rows
+        // whose merge feed backed up on exact finish-time ties (counted = -1):
+        // such a chunk is simulated again with the per-event kernel
+        if (max_chains <= 1 && max_cap <= 16 && (out_jobs || !use_seg(max_chains, max_cap, n_jobs))) {
+            std::vector<cs_rep_summary> hs((size_t)n_points * n_reps);
+            cudaMemcpyAsync(hs.data(), b_summ.p, sizeof(cs_rep_summary) * hs.size(), cudaMemcpyDeviceToHost, st);
+            if ((rc = check_cuda(cudaStreamSynchronize(st), "chunk summaries"))) return rc;
+            bool redo = false;
+            for (int32_t p = 0; p < n_points && !redo; p++)
+                for (int64_t i = 0; i < cn; i++)
+                    if (hs[(size_t)p * n_reps + c0 + i].counted < 0) redo = true;
+            if (redo &&
+                (rc = cs_jffc_sim_impl((const cs_sim_point*)b_pts.p, n_points, (const double*)b_rates.p,
+                                       (const int32_t*)b_caps.p, max_chains, max_cap, (const double*)b_S.p,
+                                       lds, (int32_t)c0, (int32_t)cn, n_reps, n_jobs, warm, (double*)b_resp.p,
+                                       ldr, (double*)b_busy.p, ldb, (cs_rep_summary*)b_summ.p,
+                                       (double*)b_jobs.p, b_ws.p, wsb, CS_SIM_FORCE_EVENT_LOOP, st)))
+                return rc;
+        }
         if (c0 + chunk < n_reps && (rc = check_cuda(cudaStreamSynchronize(st), "chunk sync"))) return rc;
     }
     rc = cs_rep_stats_impl((const double*)b_resp.p, n_points, n_reps, m, ldr, (cs_rep_summary*)b_summ.p,

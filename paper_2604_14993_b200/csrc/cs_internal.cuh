@@ -32,9 +32,11 @@ inline int check_cuda(cudaError_t e, const char* what) {
     return CS_OK;
 }
 
-// Keep freed stream-ordered allocations in the device pool instead of
-// returning them to the OS at every synchronisation (default threshold 0).
+// The engine's private stream-ordered pool (capi.cu): scratch of the
+// host-level calls comes from it; pool_alloc = cudaMallocFromPoolAsync.
 void ensure_mem_pool();
+cudaMemPool_t engine_pool();
+int pool_alloc(void** p, size_t n, cudaStream_t st);
 
 // NCCL all-reduces of the sharded statistics (dist.cu); no-ops without a
 // multi-rank communicator.

@@ -12,10 +12,13 @@
 //   * next_double(u64) = (u64 >> 11) * 2^-53.
 //   * random_standard_exponential: 256-layer ziggurat with tables
 //     we/ke/fe (zig_tables.cuh, pinned against numpy's rodata), tail
-//     r - log1p(-next_double), wedge (fe[i-1]-fe[i])*u + fe[i] < exp(-x).
+//     r - log1p(-next_double), wedge (fe[i-1]-fe[i])*u + fe[i] < exp(-x);
+//     log1p and exp are ports of the host glibc's (glibc_log1p.cuh,
+//     glibc_exp.cuh), so every accept/reject decision is the host's.
 #pragma once
 #include <stdint.h>
 
+#include "glibc_exp.cuh"
 #include "glibc_log1p.cuh"
 #include "zig_tables.cuh"
 
@@ -97,12 +100,11 @@ __device__ __noinline__ ZigAttempt zig_slow(const ZigSmem* z, uint64_t w, uint64
         a.v = __dsub_rn(r, glibc_log1p(-u, log1p_fma));
         a.has = true;
     } else {
-        // numpy: (fe[idx-1]-fe[idx]) * next_double + fe[idx] < exp(-x), no contraction.
-        // exp() is CUDA's (<= 1 ulp); a decision flip needs y to equal the 1-ulp
-        // neighbour of glibc's exp(-x): probability ~1e-15 per wedge test.
+        // numpy: (fe[idx-1]-fe[idx]) * next_double + fe[idx] < exp(-x), no
+        // contraction, exp = the host glibc's (same build variant as log1p)
         const double y = __dadd_rn(__dmul_rn(__dsub_rn(z->fe[idx - 1], z->fe[idx]), u), z->fe[idx]);
         a.v = x;
-        a.has = y < exp(-x);
+        a.has = y < glibc_exp(-x, log1p_fma);
     }
     return a;
 }

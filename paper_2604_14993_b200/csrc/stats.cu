@@ -532,7 +532,7 @@ struct DBuf {
     int alloc(size_t bytes, cudaStream_t s) {
         st = s;
         n = bytes;
-        return check_cuda(cudaMallocAsync(&p, bytes ? bytes : 16, s), "cudaMallocAsync");
+        return pool_alloc(&p, bytes, s);
     }
     template <class T>
     T* as() const {

@@ -262,19 +262,35 @@ def test_compose_batch_random_fleets_match_oracle(eng, oracle):
         assert np.array_equal(bits([ch.service_time_s for ch in sysm.chains]), bits(a["times"]))
 
 
-def test_tune_capacity_surrogate_batched(eng, golden):
-    """c in [1, c_max] evaluated in one launch equals per-c greedy placement."""
-    service, servers, _ = eng.petals_instance(10, 0.2, 101)
-    tuning = eng.tune_capacity_surrogate(servers, service, 0.2, 0.7)
-    assert len(tuning.rows) == eng.capacity_upper_bound(servers, service) == 351 - 0 or True
-    for row in tuning.rows[:40]:
-        try:
-            r = eng.greedy_block_placement(servers, service, row.capacity, 0.2, 0.7)
-        except eng.InfeasibleError:
-            assert row.chain_count is None
-            continue
-        assert row.chain_count == r.chain_count
-        assert row.rate_satisfied == r.rate_satisfied
+def _surrogate_cases():
+    import json
+    import os
+
+    with open(os.path.join(os.path.dirname(__file__), "golden", "golden_surrogate.json")) as fh:
+        return json.load(fh)["cases"]
+
+
+@pytest.mark.parametrize("case", _surrogate_cases(), ids=lambda c: c["name"])
+def test_tune_capacity_surrogate_matches_reference(eng, case):
+    """c in [1, c_max] evaluated in one GBP launch: c_star and every
+    TuningRow (placement.py:161-200) bit-exact vs the reference, or the same
+    InfeasibleError message and best_rate."""
+    servers = tuple(eng.ServerSpec(r[0], int(r[1]), float.fromhex(r[2]), float.fromhex(r[3]))
+                    for r in case["servers"])
+    service = eng.ServiceSpec(*case["service"])
+    lam, rho = float.fromhex(case["lam"]), float.fromhex(case["rho"])
+    if "infeasible" in case:
+        with pytest.raises(eng.InfeasibleError) as exc:
+            eng.tune_capacity_surrogate(servers, service, lam, rho)
+        assert str(exc.value) == case["infeasible"]
+        assert same_float(exc.value.best_rate, float.fromhex(case["best_rate"]))
+        return
+    t = eng.tune_capacity_surrogate(servers, service, lam, rho)
+    assert t.c_star == case["c_star"]
+    assert len(t.rows) == len(case["rows"])
+    for row, ref in zip(t.rows, case["rows"]):
+        assert [row.capacity, row.chain_count, row.scaled_cost, row.rate_satisfied] == ref[:4], ref
+        assert same_float(row.achieved_rate, float.fromhex(ref[4])), ref
 
 
 def test_no_silent_fallback_loaded_native(eng):
@@ -283,9 +299,9 @@ def test_no_silent_fallback_loaded_native(eng):
     assert N._lib is not None and N.LIB_PATH.endswith("libchainserve_b200.so")
 
 
-def test_sample_select_and_fused_pairwise_means(eng, oracle):
+def test_sample_select_and_pairwise_means(eng, oracle):
     """Groups above 2^20 responses take the sample-select path; per-rep means
-    come from the simulator's streamed numpy pairwise sum (bit-exact)."""
+    are the statistics pass's numpy pairwise sums (bit-exact)."""
     service, servers, _ = eng.petals_instance(10, 0.2, 101)
     system = eng.greedy_cache_allocation(
         eng.greedy_block_placement(servers, service, 7, 0.2, 0.7).placement)
@@ -368,3 +384,47 @@ def test_single_chain_kernel_stress(eng, oracle, C):
                 assert same_float(res.busy[p][r, 0], o["busy_time_s"][0]), (p, r)
                 for f in REP_FIELDS:
                     assert same_float(res.summaries[p, r][f], o[f]), (p, r, f)
+
+
+def test_event_loop_fallback_equals_recursion(eng, oracle, monkeypatch):
+    """CS_SIM_FORCE_EVENT_LOOP (the per-event register kernel the host path
+    falls back to when the serial recursion kernel reports a backed-up merge)
+    gives the same bits as the recursion kernel and the oracle."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2604_14993_b200 import _native as N
+
+    monkeypatch.setenv("CS_SIM_EXACT", "1")
+    lib = N.load()
+    rates, caps = (0.8,), (5,)
+    lams = [0.5 * 4.0, 0.97 * 4.0]
+    n, warm, R, P = 8000, 800, 6, 2
+    keys = np.concatenate([oracle.philox_key(3, r) for r in range(R)]).astype(np.uint64)
+    d_keys = torch.from_numpy(keys.view(np.int64)).cuda()
+    pts = (N.SimPoint * P)(*[N.SimPoint(1, 0, l) for l in lams])
+    d_pts = torch.frombuffer(bytearray(bytes(pts)), dtype=torch.uint8).cuda()
+    d_rates = torch.tensor(rates, dtype=torch.float64, device="cuda")
+    d_caps = torch.tensor(caps, dtype=torch.int32, device="cuda")
+    lds, ldr = 2 * n, (n - warm + 15) & ~15
+    S = torch.empty(R * lds + 512, dtype=torch.float64, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    N.check(lib.cs_exp_streams(d_keys.data_ptr(), R, lds, S.data_ptr(), lds, -1, st), "streams")
+    outs = []
+    for flags in (0, N.CS_SIM_FORCE_EVENT_LOOP):
+        resp = torch.zeros(P * R * ldr, dtype=torch.float64, device="cuda")
+        busy = torch.zeros(P * R, dtype=torch.float64, device="cuda")
+        summ = torch.zeros(P * R * C.sizeof(N.RepSummary), dtype=torch.uint8, device="cuda")
+        N.check(lib.cs_jffc_sim_ex(d_pts.data_ptr(), P, d_rates.data_ptr(), d_caps.data_ptr(), 1, 5,
+                                   S.data_ptr(), lds, 0, R, R, n, warm, resp.data_ptr(), ldr,
+                                   busy.data_ptr(), 1, summ.data_ptr(), None, None, 0, flags, st), "sim")
+        outs.append((resp.cpu().numpy().reshape(P, R, ldr)[:, :, :n - warm], busy.cpu().numpy(),
+                     summ.cpu().numpy().view(N.SUMMARY_DTYPE).reshape(P, R)))
+    assert np.array_equal(bits(outs[0][0]), bits(outs[1][0]))
+    assert np.array_equal(bits(outs[0][1]), bits(outs[1][1]))
+    for f in REP_FIELDS:
+        assert np.array_equal(bits(outs[0][2][f].astype(np.float64)), bits(outs[1][2][f].astype(np.float64))), f
+    for p in range(P):
+        resp, _, _ = oracle.simulate_reps(rates, caps, lams[p], n, 0.1, 3, 0, R)
+        assert np.array_equal(bits(outs[1][0][p]), bits(resp)), p
