@@ -32,15 +32,19 @@ struct Xfer {
 // of its warp (p < P, the sweep points sharing the stream) runs the exact
 // sequential cumsum a_j = a_{j-1} + (1/lam_p) * S_j of np.cumsum and records
 // a_j at the listed job indices into out[(r * P + p) * ncol + col].
+// streams (warps) per block; each warp's chunk loop is latency-bound, so the
+// block shape barely matters (4 per block measured 2% slower than 8)
+constexpr int EXP_WARPS = 8;
+
 template <bool PFX>
-__global__ void __launch_bounds__(256) exp_streams_kernel(const uint64_t* __restrict__ keys,
+__global__ void __launch_bounds__(EXP_WARPS * 32) exp_streams_kernel(const uint64_t* __restrict__ keys,
                                                           int64_t n_streams, int64_t n_draws,
                                                           double* __restrict__ out, int64_t ld,
                                                           int log1p_fma,
                                                           int64_t* __restrict__ words_used,
                                                           const PrefixPlan pp) {
     __shared__ ZigSmem zs;
-    __shared__ double sh_vals[PFX ? 8 : 1][136];  // a chunk's values (<= 128 + carry), per warp
+    __shared__ double sh_vals[PFX ? EXP_WARPS : 1][136];  // a chunk's values (<= 128 + carry), per warp
     zig_load(&zs);
     __syncthreads();
     const int lane = threadIdx.x & 31;
@@ -248,7 +252,7 @@ extern "C" int cs_philox_peak_impl(int64_t blocks_per_thread, int32_t grid, uint
 extern "C" int cs_exp_streams_impl(const uint64_t* d_keys, int64_t n_streams, int64_t n_draws,
                                    double* d_out, int64_t ld, int log1p_fma, void* stream) {
     if (n_streams <= 0 || n_draws <= 0) return 0;
-    const int warps_per_block = 8;
+    const int warps_per_block = cs::EXP_WARPS;
     const int64_t blocks = (n_streams + warps_per_block - 1) / warps_per_block;
     cs::PrefixPlan none{};
     cs::exp_streams_kernel<false><<<(unsigned)blocks, warps_per_block * 32, 0, (cudaStream_t)stream>>>(
@@ -261,7 +265,7 @@ extern "C" int cs_exp_streams_prefix_impl(const uint64_t* d_keys, int64_t n_stre
                                           double* d_out, int64_t ld, int log1p_fma,
                                           const cs::PrefixPlan* plan, void* stream) {
     if (n_streams <= 0 || n_draws <= 0) return 0;
-    const int warps_per_block = 8;
+    const int warps_per_block = cs::EXP_WARPS;
     const int64_t blocks = (n_streams + warps_per_block - 1) / warps_per_block;
     cs::exp_streams_kernel<true><<<(unsigned)blocks, warps_per_block * 32, 0, (cudaStream_t)stream>>>(
         d_keys, n_streams, n_draws, d_out, ld, log1p_fma, nullptr, *plan);
