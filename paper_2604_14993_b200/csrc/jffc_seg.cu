@@ -261,8 +261,13 @@ __global__ void __launch_bounds__(32) seg_prefix_kernel(Args A) {
 // ---------------------------------------------------------------------------
 enum { PH_A = 0, PH_B = 1, PH_C = 2 };  // before warm-up / first / second half of the window
 
+// <= 128 registers: 16 warps per SM (measured against 20 and 24 warps with
+// spills: 13.6 / 14.7 / 17.8 ms on config 2; without the bound ptxas took 144)
+#ifndef CS_SEG_MINB
+#define CS_SEG_MINB 16
+#endif
 template <int CMAX>
-__global__ void __launch_bounds__(32) jffc_seg_kernel(Args A) {
+__global__ void __launch_bounds__(32, CS_SEG_MINB) jffc_seg_kernel(Args A) {
     constexpr int ID_BITS = CMAX <= 8 ? 3 : 4;
     constexpr uint32_t DUMMY = 0x80000000u;  // an initially idle slot, not a job
     constexpr uint32_t J_MASK = (1u << (31 - ID_BITS)) - 1;
