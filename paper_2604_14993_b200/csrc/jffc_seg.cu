@@ -137,6 +137,17 @@ __device__ __forceinline__ void st_v2(double* p, double x, double y) {
     asm volatile("st.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(x), "d"(y) : "memory");
 }
 __device__ __forceinline__ double dmax0(double x) { return x > 0.0 ? x : 0.0; }
+// explicit shared-window accesses (32-bit addresses: no generic-to-shared
+// conversion on the per-job path)
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ double lds_f64(uint32_t a) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts_f64(uint32_t a, double v) {
+    asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+}
 
 // ---------------------------------------------------------------------------
 // Pre-pass: the exact arrival times at the segment starts and at the
@@ -266,6 +277,10 @@ enum { PH_A = 0, PH_B = 1, PH_C = 2 };  // before warm-up / first / second half 
 #ifndef CS_SEG_MINB
 #define CS_SEG_MINB 16
 #endif
+#ifndef CS_SEG_UNROLL
+#define CS_SEG_UNROLL 4  // measured on config 2: 1 11.77, 2 11.83, 4 11.10 ms
+#endif
+constexpr int SEG_UNROLL = CS_SEG_UNROLL;  // jobs per trip of the step loops
 template <int CMAX>
 __global__ void __launch_bounds__(32, CS_SEG_MINB) jffc_seg_kernel(Args A) {
     constexpr int ID_BITS = CMAX <= 8 ? 3 : 4;
@@ -275,8 +290,8 @@ __global__ void __launch_bounds__(32, CS_SEG_MINB) jffc_seg_kernel(Args A) {
     constexpr int FCK = CMAX + 1;
     constexpr unsigned FULL = 0xffffffffu;
 
-    // response ring: element (pos, lane) at [(pos >> 1) & 15][lane][pos & 1], row pitch 66 doubles
-    __shared__ __align__(16) double sh_ring[16 * 66];
+    // response ring: element (pos, lane) at [pos & 31][lane], row pitch 33 doubles
+    __shared__ __align__(16) double sh_ring[32 * 33];
     __shared__ double sh_rbuf[CMAX * 32];  // response of the job holding slot id
     __shared__ double* sh_row[32];         // response row of each lane
     __shared__ int4 sh_meta[32];           // per-lane flush line: start, first, end, has
@@ -316,7 +331,8 @@ __global__ void __launch_bounds__(32, CS_SEG_MINB) jffc_seg_kernel(Args A) {
         fin[k] = k < cap ? -INFINITY : INFINITY;
         key[k] = DUMMY | (uint32_t)k;
     }
-    double* rbuf = sh_rbuf + lane;
+    const uint32_t rbuf_a = smem_addr(sh_rbuf + lane);  // slot id k at + k * 256
+    const uint32_t ring_a = smem_addr(sh_ring + lane);  // position p at + (p & 31) * 264
     // positions are < n - warm < 2^27: 32-bit
     int32_t n_resp = (int32_t)(b > warm ? b - warm : 0);  // counted jobs before b = the exact position at coupling
     int32_t fl_lo = n_resp;                               // first position not yet flushed
@@ -326,7 +342,7 @@ __global__ void __launch_bounds__(32, CS_SEG_MINB) jffc_seg_kernel(Args A) {
     bool act = valid;  // lane simulates / writes / accumulates
 
     int32_t j = (int32_t)b;
-    const int32_t warm32 = (int32_t)warm;
+    const int32_t warm_key = (int32_t)warm << ID_BITS;
     double a = pre[s];  // a_b
     const double* __restrict__ gp = gap + b + 1;  // gap of job j+1
     const double* __restrict__ sp = szs + b;      // size of job j
@@ -334,9 +350,7 @@ __global__ void __launch_bounds__(32, CS_SEG_MINB) jffc_seg_kernel(Args A) {
     __syncwarp();
 
     // ---- helpers (warp-uniform control flow) ---------------------------
-    auto ring_put = [&](int32_t pos, double v) {
-        sh_ring[((pos >> 1) & 15) * 66 + 2 * lane + (pos & 1)] = v;
-    };
+    auto ring_put = [&](int32_t pos, double v) { sts_f64(ring_a + (uint32_t)(pos & 31) * 264u, v); };
     // flush complete lines (final: also the trailing partial line) of the
     // lanes in `who`; lines go out 4 per warp instruction, 8 threads x 16 B
     // each; the first and last line of a lane's range element by element.
@@ -359,8 +373,7 @@ __global__ void __launch_bounds__(32, CS_SEG_MINB) jffc_seg_kernel(Args A) {
                     const int4 md = sh_meta[L];
                     if (md.w) {
                         const int32_t p0 = md.x + 2 * c;
-                        const double2 v =
-                            *reinterpret_cast<const double2*>(&sh_ring[((p0 >> 1) & 15) * 66 + 2 * L]);
+                        const double2 v = make_double2(sh_ring[(p0 & 31) * 33 + L], sh_ring[((p0 + 1) & 31) * 33 + L]);
                         double* dst = sh_row[L] + p0;
                         if (p0 >= md.y && p0 + 1 < md.z) {
                             st_v2(dst, v.x, v.y);
@@ -385,23 +398,26 @@ __global__ void __launch_bounds__(32, CS_SEG_MINB) jffc_seg_kernel(Args A) {
 
     // one job (step j) of the recursion; PH picks the sums' form, act_l
     // predicates emission and sums on the lane's active flag
-    auto step = [&](auto ph_tag, bool act_l) {
+    // (every lane steps; an inactive lane's results are never stored: its
+    // flushes and block sums are gated on its active flag)
+    auto step = [&](auto ph_tag) {
         constexpr int PH = decltype(ph_tag)::value;
         const double m = fin[0];
         const uint32_t k0 = key[0];
-        const uint32_t id = k0 & ID_MASK;
-        const double rv = rbuf[id * 32];  // response of the slot's previous job
+        const uint32_t ra = rbuf_a + (k0 & ID_MASK) * 256u;
+        const double rv = lds_f64(ra);  // response of the slot's previous job
         const double aj = a;
         const double st = m <= aj ? aj : m;
         const double d = __dmul_rn(sz, inv_mu);
         const double f = __dadd_rn(st, d);
         const double rr = __dsub_rn(f, aj);
-        const bool counted = act_l && !(k0 & DUMMY) && (int32_t)((k0 >> ID_BITS) & J_MASK) >= warm32;
+        // a real job (dummies are negative) of index >= warm: key >= warm << ID_BITS
+        const bool counted = (int32_t)k0 >= warm_key;
         ring_put(n_resp, rv);  // slot n_resp is free (< 32 unflushed): kept only if counted
         n_resp += counted;
-        rbuf[id * 32] = rr;
+        sts_f64(ra, rr);
         // remove W[0], insert (f, j): equal finish goes after (larger job index)
-        const uint32_t nk = ((uint32_t)j << ID_BITS) | id;
+        const uint32_t nk = ((uint32_t)j << ID_BITS) | (k0 & ID_MASK);
         bool lt[CMAX];
 #pragma unroll
         for (int k = 0; k < CMAX - 1; k++) lt[k] = fin[k + 1] <= f;
@@ -428,7 +444,7 @@ __global__ void __launch_bounds__(32, CS_SEG_MINB) jffc_seg_kernel(Args A) {
         // window's end (rare: in system at mid / at the last arrival) take
         // the clipped form, the rest the plain one
         if (PH == PH_A) {  // a <= w_start: clipped on both sides
-            if (act_l) {
+            {
                 const bool fe = f <= Te;
                 const double he = fe ? f : Te;
                 const double hm = f <= Tm ? f : Tm;
@@ -439,9 +455,9 @@ __global__ void __launch_bounds__(32, CS_SEG_MINB) jffc_seg_kernel(Args A) {
                 ag[AG_ENDQ] += st > Te ? 1.0 : 0.0;
             }
         } else {
-            const bool slow = act_l && f > (PH == PH_B ? Tm : Te);
+            const bool slow = f > (PH == PH_B ? Tm : Te);
             if (__any_sync(FULL, slow)) {
-                if (act_l) {
+                {
                     const bool fe = f <= Te;
                     ag[AG_WAIT] = __dadd_rn(ag[AG_WAIT], __dsub_rn(st, aj));
                     ag[AG_SERV] = __dadd_rn(ag[AG_SERV], d);
@@ -450,7 +466,7 @@ __global__ void __launch_bounds__(32, CS_SEG_MINB) jffc_seg_kernel(Args A) {
                     if (PH == PH_B) ag[AG_AMID] = __dadd_rn(ag[AG_AMID], f <= Tm ? rr : __dsub_rn(Tm, aj));
                     ag[AG_ENDQ] += st > Te ? 1.0 : 0.0;
                 }
-            } else if (act_l) {  // f <= T: the plain intervals
+            } else {  // f <= T: the plain intervals
                 ag[AG_WAIT] = __dadd_rn(ag[AG_WAIT], __dsub_rn(st, aj));
                 ag[AG_SERV] = __dadd_rn(ag[AG_SERV], d);
                 ag[AG_AEND] = __dadd_rn(ag[AG_AEND], rr);
@@ -464,20 +480,20 @@ __global__ void __launch_bounds__(32, CS_SEG_MINB) jffc_seg_kernel(Args A) {
     using TC = std::integral_constant<int, PH_C>;
     // up to 16 steps to jn (a multiple of 16 or the range end), split at the
     // warm-up and mid indices
-    auto run_to = [&](int64_t jn, bool act_l) {
+    auto run_to = [&](int64_t jn) {
         while (j < jn) {
             if (j < warm) {
                 const int cnt = (int)((warm < jn ? warm : jn) - j);
-#pragma unroll 2
-                for (int k = 0; k < cnt; k++) step(TA(), act_l);
+#pragma unroll SEG_UNROLL
+                for (int k = 0; k < cnt; k++) step(TA());
             } else if (j < mid) {
                 const int cnt = (int)((mid < jn ? mid : jn) - j);
-#pragma unroll 2
-                for (int k = 0; k < cnt; k++) step(TB(), act_l);
+#pragma unroll SEG_UNROLL
+                for (int k = 0; k < cnt; k++) step(TB());
             } else {
                 const int cnt = (int)(jn - j);
-#pragma unroll 2
-                for (int k = 0; k < cnt; k++) step(TC(), act_l);
+#pragma unroll SEG_UNROLL
+                for (int k = 0; k < cnt; k++) step(TC());
             }
         }
     };
@@ -487,7 +503,7 @@ __global__ void __launch_bounds__(32, CS_SEG_MINB) jffc_seg_kernel(Args A) {
             const uint32_t kk = key[k];
             const bool counted = act_l && !(kk & DUMMY) && fin[k] < INFINITY &&
                                  (int64_t)((kk >> ID_BITS) & J_MASK) >= warm;
-            if (counted) ring_put(n_resp, rbuf[(kk & ID_MASK) * 32]);
+            if (counted) ring_put(n_resp, lds_f64(rbuf_a + (kk & ID_MASK) * 256u));
             n_resp += counted;
         }
     };
@@ -512,7 +528,7 @@ __global__ void __launch_bounds__(32, CS_SEG_MINB) jffc_seg_kernel(Args A) {
         while (j < e) {
             const int64_t jn = (j + 16 < e) ? j + 16 : e;  // b is a multiple of BS
             prefetch();
-            run_to(jn, act);
+            run_to(jn);
             flush(false, act);
             if (j % (int32_t)BS == 0 || j == n) put_block(act);
             if (j == next_ck) {
@@ -571,7 +587,7 @@ __global__ void __launch_bounds__(32, CS_SEG_MINB) jffc_seg_kernel(Args A) {
         while (j < et && __any_sync(FULL, act)) {
             const int64_t jn = (j + 16 < et) ? j + 16 : et;
             prefetch();
-            run_to(jn, act);
+            run_to(jn);
             flush(false, act);
             if (j % (int32_t)BS == 0 || j == n) put_block(act);
             if (j == next_ck) {
