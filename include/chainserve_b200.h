@@ -133,9 +133,14 @@ int64_t cs_jffc_sim_workspace_bytes(int32_t n_points, int32_t n_reps, int32_t ma
  * segmented single-chain path applies (and n_points <= 32), the stream kernel
  * also runs the exact arrival-time cumsum of every (replication, point) row
  * and records the simulator's per-segment start times into d_workspace
- * (sized by cs_jffc_sim_workspace_bytes); *prefix_ready is then 1 and the
- * simulation call takes flags CS_SIM_PREFIX_READY (it skips its own pre-pass). */
+ * (sized by cs_jffc_sim_workspace_bytes).  *sim_flags receives the flags the
+ * simulation call must take: CS_SIM_PREFIX_READY (it skips its own pre-pass)
+ * and, with fewer than 16 points per stream (n_streams a multiple of 32, ld of
+ * 4), CS_SIM_STREAMS_IL4: d_out then holds the streams in the simulator's
+ * 32-row interleaved layout (stream r's value i at (r/32)*32*ld + (i/4)*128 +
+ * (r%32)*4 + i%4), readable by the segmented simulator only. */
 #define CS_SIM_PREFIX_READY 1
+#define CS_SIM_STREAMS_IL4 4
 /* cs_jffc_sim_ex: take the per-event register kernel for single-chain
  * compositions instead of the serial recursion kernel (its fallback when
  * exact finish-time ties back up the recursion's merge feed: counted = -1) */
@@ -143,10 +148,11 @@ int64_t cs_jffc_sim_workspace_bytes(int32_t n_points, int32_t n_reps, int32_t ma
 int cs_sim_streams(const uint64_t* d_keys, int64_t n_streams, int64_t n_draws, double* d_out, int64_t ld,
                    int32_t log1p_variant, const cs_sim_point* d_points, int32_t n_points,
                    int32_t max_chains, int32_t max_capacity, int64_t n_jobs, int64_t warm,
-                   void* d_workspace, int64_t workspace_bytes, int32_t* prefix_ready, void* stream);
+                   void* d_workspace, int64_t workspace_bytes, int32_t* sim_flags, void* stream);
 
 /* cs_jffc_sim with flags (CS_SIM_PREFIX_READY: d_workspace holds the prefix
- * cs_sim_streams wrote for exactly these streams and shape). */
+ * cs_sim_streams wrote for exactly these streams and shape; CS_SIM_STREAMS_IL4:
+ * d_streams is in the interleaved layout; pass cs_sim_streams' *sim_flags). */
 int cs_jffc_sim_ex(const cs_sim_point* d_points, int32_t n_points, const double* d_rates,
                    const int32_t* d_caps, int32_t max_chains, int32_t max_capacity,
                    const double* d_streams, int64_t lds, int32_t rep_begin, int32_t n_reps,

@@ -17,6 +17,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libchainser
 
 CS_OK, CS_INFEASIBLE, CS_INVALID, CS_INTERNAL, CS_ERR_CUDA, CS_UNSUPPORTED, CS_UNSTABLE = range(7)
 CS_SIM_PREFIX_READY = 1
+CS_SIM_STREAMS_IL4 = 4
 CS_SIM_FORCE_EVENT_LOOP = 2
 
 

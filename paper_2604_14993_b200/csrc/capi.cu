@@ -18,7 +18,7 @@ extern "C" int cs_jffc_sim_impl(const cs_sim_point*, int32_t, const double*, con
                                 int64_t, double*, int64_t, double*, int32_t, cs_rep_summary*, double*,
                                 void*, int64_t, int32_t, void*);
 extern "C" int cs_exp_streams_prefix_impl(const uint64_t*, int64_t, int64_t, double*, int64_t, int,
-                                          const cs::PrefixPlan*, void*);
+                                          const cs::PrefixPlan*, int, void*);
 extern "C" bool cs_seg_prefix_plan(int32_t, int32_t, int32_t, int64_t, int64_t, const cs_sim_point*, void*,
                                    cs::PrefixPlan*);
 namespace cs {
@@ -221,6 +221,10 @@ int cs_jffc_sim_ex(const cs_sim_point* d_points, int32_t n_points, const double*
         set_error("cs_jffc_sim: invalid sizes");
         return CS_INVALID;
     }
+    if ((flags & CS_SIM_STREAMS_IL4) && (d_jobs != nullptr || !cs::use_seg(max_chains, max_capacity, n_jobs))) {
+        set_error("cs_jffc_sim: interleaved streams are read by the segmented path only");
+        return CS_INVALID;
+    }
     return cs_jffc_sim_impl(d_points, n_points, d_rates, d_caps, max_chains, max_capacity, d_streams,
                             lds, rep_begin, n_reps, n_reps_total, n_jobs, warm, d_responses, ldr,
                             d_busy, ldb, d_summary, d_jobs, d_workspace, workspace_bytes, flags, stream);
@@ -240,8 +244,8 @@ int cs_jffc_sim(const cs_sim_point* d_points, int32_t n_points, const double* d_
 int cs_sim_streams(const uint64_t* d_keys, int64_t n_streams, int64_t n_draws, double* d_out, int64_t ld,
                    int32_t log1p_variant, const cs_sim_point* d_points, int32_t n_points,
                    int32_t max_chains, int32_t max_capacity, int64_t n_jobs, int64_t warm,
-                   void* d_workspace, int64_t workspace_bytes, int32_t* prefix_ready, void* stream) {
-    if (prefix_ready) *prefix_ready = 0;
+                   void* d_workspace, int64_t workspace_bytes, int32_t* sim_flags, void* stream) {
+    if (sim_flags) *sim_flags = 0;
     if (cs_device_count() == 0) {
         set_error("cs_sim_streams: no CUDA device");
         return CS_ERR_CUDA;
@@ -254,10 +258,12 @@ int cs_sim_streams(const uint64_t* d_keys, int64_t n_streams, int64_t n_draws, d
     cs::PrefixPlan pp;
     const int64_t need = cs_jffc_sim_workspace_bytes_impl(n_points, (int32_t)n_streams, max_chains,
                                                           max_capacity, n_jobs);
-    if (prefix_ready && d_workspace && workspace_bytes >= need && cs::use_seg(max_chains, max_capacity, n_jobs) &&
+    if (sim_flags && d_workspace && workspace_bytes >= need && cs::use_seg(max_chains, max_capacity, n_jobs) &&
         cs_seg_prefix_plan(n_points, (int32_t)n_streams, max_capacity, n_jobs, warm, d_points, d_workspace, &pp)) {
-        const int rc = cs_exp_streams_prefix_impl(d_keys, n_streams, n_draws, d_out, ld, v, &pp, stream);
-        if (rc == CS_OK) *prefix_ready = 1;
+        // few points per stream: every simulator lane reads its own row
+        const bool il4 = n_points < 16 && n_streams % 32 == 0 && ld % 4 == 0;
+        const int rc = cs_exp_streams_prefix_impl(d_keys, n_streams, n_draws, d_out, ld, v, &pp, il4, stream);
+        if (rc == CS_OK) *sim_flags = CS_SIM_PREFIX_READY | (il4 ? CS_SIM_STREAMS_IL4 : 0);
         return rc;
     }
     return cs_exp_streams_impl(d_keys, n_streams, n_draws, d_out, ld, v, stream);
@@ -399,17 +405,17 @@ int cs_run_sim_host(const cs_sim_point* points, int32_t n_points, const double* 
         if ((rc = cs_philox_keys(entropy, n_entropy, reps.data(), cn, keys.data()))) return rc;
         // the host vector is reused next chunk: order the copy before it
         cudaMemcpyAsync(b_keys.p, keys.data(), sizeof(uint64_t) * 2 * cn, cudaMemcpyHostToDevice, st);
-        int32_t ready = 0;
+        int32_t sim_flags = 0;
         if ((rc = cs_sim_streams((const uint64_t*)b_keys.p, cn, lds, (double*)b_S.p, lds, log1p_variant,
                                  (const cs_sim_point*)b_pts.p, n_points, max_chains, max_cap, n_jobs, warm,
-                                 out_jobs ? nullptr : b_ws.p, wsb, &ready, st)))
+                                 out_jobs ? nullptr : b_ws.p, wsb, &sim_flags, st)))
             return rc;
         if ((rc = cs_jffc_sim_impl((const cs_sim_point*)b_pts.p, n_points, (const double*)b_rates.p,
                                    (const int32_t*)b_caps.p, max_chains, max_cap, (const double*)b_S.p,
                                    lds, (int32_t)c0, (int32_t)cn, n_reps, n_jobs, warm,
                                    (double*)b_resp.p, ldr, (double*)b_busy.p, ldb,
                                    (cs_rep_summary*)b_summ.p, (double*)b_jobs.p, b_ws.p, wsb,
-                                   ready ? CS_SIM_PREFIX_READY : 0, st)))
+                                   sim_flags, st)))
             return rc;
         // the serial single-chain kernel (exact mode / job records) flags rows
         // whose merge feed backed up on exact finish-time ties (counted = -1):

@@ -36,7 +36,10 @@ struct Xfer {
 // block shape barely matters (4 per block measured 2% slower than 8)
 constexpr int EXP_WARPS = 8;
 
-template <bool PFX>
+// IL4 (with PFX only): the output in the simulator's interleaved layout
+// (jffc_seg.cu il4_off): stream r's value i at (r / 32) * 32 * ld +
+// (i / 4) * 128 + (r % 32) * 4 + i % 4, written from the chunk buffer.
+template <bool PFX, bool IL4>
 __global__ void __launch_bounds__(EXP_WARPS * 32) exp_streams_kernel(const uint64_t* __restrict__ keys,
                                                           int64_t n_streams, int64_t n_draws,
                                                           double* __restrict__ out, int64_t ld,
@@ -51,7 +54,7 @@ __global__ void __launch_bounds__(EXP_WARPS * 32) exp_streams_kernel(const uint6
     const int64_t stream = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (stream >= n_streams) return;
     const uint64_t k0 = keys[2 * stream], k1 = keys[2 * stream + 1];
-    double* __restrict__ o = out + stream * ld;
+    double* __restrict__ o = IL4 ? out + (stream >> 5) * 32 * ld + (stream & 31) * 4 : out + stream * ld;
     double* cv = sh_vals[PFX ? (threadIdx.x >> 5) : 0];
     // prefix state: lane p handles point p (P <= 32 per pass; more points loop)
     double pa[PFX ? PrefixPlan::MAXP32 : 1];
@@ -156,7 +159,7 @@ __global__ void __launch_bounds__(EXP_WARPS * 32) exp_streams_kernel(const uint6
         // Emit this lane's values.
         int64_t base = produced + pos;
         if (carry_has) {
-            if (base < n_draws) o[base] = carry_v;
+            if (!IL4 && base < n_draws) o[base] = carry_v;
             if (PFX) cv[base - produced] = carry_v;
             base++;
         }
@@ -166,7 +169,7 @@ __global__ void __launch_bounds__(EXP_WARPS * 32) exp_streams_kernel(const uint6
             for (int q = 0; q < 4; q++)
                 if (p == q) {
                     if (has[q]) {
-                        if (base < n_draws) o[base] = v[q];
+                        if (!IL4 && base < n_draws) o[base] = v[q];
                         if (PFX) cv[base - produced] = v[q];
                         base++;
                     }
@@ -177,6 +180,13 @@ __global__ void __launch_bounds__(EXP_WARPS * 32) exp_streams_kernel(const uint6
         const int tot = __shfl_sync(0xffffffffu, entry ? inc.c1 : inc.c0, 31);
         const int nxt = __shfl_sync(0xffffffffu, entry ? inc.x1 : inc.x0, 31);
         pend_w = __shfl_sync(0xffffffffu, w[3], 31);
+        if (IL4) {  // the chunk's values in order: 4-value sectors of this row
+            __syncwarp();
+            for (int i = lane; i < tot; i += 32) {
+                const int64_t q = produced + i;
+                if (q < n_draws) o[((q >> 2) << 7) + (q & 3)] = cv[i];
+            }
+        }
         if (PFX && produced < pp.n_cum) {
             __syncwarp();
             const int cnt = (int)min((int64_t)tot, pp.n_cum - produced);
@@ -255,7 +265,7 @@ extern "C" int cs_exp_streams_impl(const uint64_t* d_keys, int64_t n_streams, in
     const int warps_per_block = cs::EXP_WARPS;
     const int64_t blocks = (n_streams + warps_per_block - 1) / warps_per_block;
     cs::PrefixPlan none{};
-    cs::exp_streams_kernel<false><<<(unsigned)blocks, warps_per_block * 32, 0, (cudaStream_t)stream>>>(
+    cs::exp_streams_kernel<false, false><<<(unsigned)blocks, warps_per_block * 32, 0, (cudaStream_t)stream>>>(
         d_keys, n_streams, n_draws, d_out, ld, log1p_fma, nullptr, none);
     return cs::check_launch("exp_streams_kernel");
 }
@@ -263,11 +273,15 @@ extern "C" int cs_exp_streams_impl(const uint64_t* d_keys, int64_t n_streams, in
 // Streams plus the segmented simulator's arrival-time prefix (jffc_seg.cu).
 extern "C" int cs_exp_streams_prefix_impl(const uint64_t* d_keys, int64_t n_streams, int64_t n_draws,
                                           double* d_out, int64_t ld, int log1p_fma,
-                                          const cs::PrefixPlan* plan, void* stream) {
+                                          const cs::PrefixPlan* plan, int il4, void* stream) {
     if (n_streams <= 0 || n_draws <= 0) return 0;
     const int warps_per_block = cs::EXP_WARPS;
     const int64_t blocks = (n_streams + warps_per_block - 1) / warps_per_block;
-    cs::exp_streams_kernel<true><<<(unsigned)blocks, warps_per_block * 32, 0, (cudaStream_t)stream>>>(
-        d_keys, n_streams, n_draws, d_out, ld, log1p_fma, nullptr, *plan);
+    if (il4)
+        cs::exp_streams_kernel<true, true><<<(unsigned)blocks, warps_per_block * 32, 0, (cudaStream_t)stream>>>(
+            d_keys, n_streams, n_draws, d_out, ld, log1p_fma, nullptr, *plan);
+    else
+        cs::exp_streams_kernel<true, false><<<(unsigned)blocks, warps_per_block * 32, 0, (cudaStream_t)stream>>>(
+            d_keys, n_streams, n_draws, d_out, ld, log1p_fma, nullptr, *plan);
     return cs::check_launch("exp_streams_kernel<prefix>");
 }

@@ -84,8 +84,9 @@ struct Args {
     const cs_sim_point* pts;
     const double* rates;
     const int32_t* caps;
-    const double* S;  // streams [R][lds]
+    const double* S;  // streams [R][lds], or the interleaved layout (il4)
     int64_t lds;
+    int32_t il4;      // streams in the 32-row sector-interleaved layout (see below)
     int32_t P, R, RT, rb;
     int64_t n, warm;
     double* resp;
@@ -281,7 +282,17 @@ enum { PH_A = 0, PH_B = 1, PH_C = 2 };  // before warm-up / first / second half 
 #define CS_SEG_UNROLL 4  // measured on config 2: 1 11.77, 2 11.83, 4 11.10 ms
 #endif
 constexpr int SEG_UNROLL = CS_SEG_UNROLL;  // jobs per trip of the step loops
-template <int CMAX>
+// Stream layouts.  Row-major [R][lds] serves warps whose lanes share a few
+// rows (P >= 16 points per stream: one L1 line per row feeds 16 jobs).  With
+// few points per stream every lane reads its own row and 32 rows x 2 streams
+// of live 128-byte lines per warp overflow L1 at 16 warps per SM; the
+// interleaved layout (cs_sim_streams picks it) stores 32 consecutive rows as
+// one group with each row's values in 4-value sectors side by side:
+// element (r, i) at (r / 32) * 32 * lds + (i / 4) * 128 + (r % 32) * 4 + i % 4,
+// so a warp's step reads 8 lines, each consumed within 4 steps.
+__device__ __forceinline__ int64_t il4_off(int64_t i) { return ((i >> 2) << 7) + (i & 3); }
+
+template <int CMAX, bool IL4>
 __global__ void __launch_bounds__(32, CS_SEG_MINB) jffc_seg_kernel(Args A) {
     constexpr int ID_BITS = CMAX <= 8 ? 3 : 4;
     constexpr uint32_t DUMMY = 0x80000000u;  // an initially idle slot, not a job
@@ -310,8 +321,9 @@ __global__ void __launch_bounds__(32, CS_SEG_MINB) jffc_seg_kernel(Args A) {
     const double inv_mu = __ddiv_rn(1.0, A.rates[pt.chain_base]);
     const int32_t cap = A.caps[pt.chain_base];
     const double scale = __ddiv_rn(1.0, pt.lam);
-    const double* __restrict__ gap = A.S + (int64_t)r * A.lds;
-    const double* __restrict__ szs = gap + n;
+    const double* __restrict__ gap =
+        IL4 ? A.S + (int64_t)(r >> 5) * 32 * A.lds + (r & 31) * 4 : A.S + (int64_t)r * A.lds;
+    const double* __restrict__ szs = gap + n;  // row-major only
     const double* pre = A.prefix + te * (S + 3);
     const double Ws = pre[S], Tm = pre[S + 1], Te = pre[S + 2];
     sh_row[lane] = (A.resp && valid) ? A.resp + o * A.ldr : nullptr;
@@ -344,9 +356,17 @@ __global__ void __launch_bounds__(32, CS_SEG_MINB) jffc_seg_kernel(Args A) {
     int32_t j = (int32_t)b;
     const int32_t warm_key = (int32_t)warm << ID_BITS;
     double a = pre[s];  // a_b
-    const double* __restrict__ gp = gap + b + 1;  // gap of job j+1
-    const double* __restrict__ sp = szs + b;      // size of job j
-    double g1 = __ldg(gp), g2 = __ldg(gp + 1), sz = __ldg(sp), sz1 = __ldg(sp + 1);
+    const double* __restrict__ gp = gap + b + 1;  // gap of job j+1 (row-major)
+    const double* __restrict__ sp = szs + b;      // size of job j (row-major)
+    double g1, g2, sz, sz1;
+    if (IL4) {
+        g1 = __ldg(gap + il4_off(b + 1));
+        g2 = __ldg(gap + il4_off(b + 2));
+        sz = __ldg(gap + il4_off(n + b));
+        sz1 = __ldg(gap + il4_off(n + b + 1));
+    } else {
+        g1 = __ldg(gp), g2 = __ldg(gp + 1), sz = __ldg(sp), sz1 = __ldg(sp + 1);
+    }
     __syncwarp();
 
     // ---- helpers (warp-uniform control flow) ---------------------------
@@ -390,10 +410,15 @@ __global__ void __launch_bounds__(32, CS_SEG_MINB) jffc_seg_kernel(Args A) {
     };
     // the next stream lines into L1 and a few ahead into L2, once per 16 jobs
     auto prefetch = [&]() {
-        prefetch_l1_if(sp + 16, true);
-        prefetch_l1_if(gp + 16, true);
-        prefetch_l2_if(sp + 80, true);
-        prefetch_l2_if(gp + 80, true);
+        if (IL4) {
+            prefetch_l2_if(gap + il4_off(n + j + 80), true);
+            prefetch_l2_if(gap + il4_off(j + 80), true);
+        } else {
+            prefetch_l1_if(sp + 16, true);
+            prefetch_l1_if(gp + 16, true);
+            prefetch_l2_if(sp + 80, true);
+            prefetch_l2_if(gp + 80, true);
+        }
     };
 
     // one job (step j) of the recursion; PH picks the sums' form, act_l
@@ -434,10 +459,15 @@ __global__ void __launch_bounds__(32, CS_SEG_MINB) jffc_seg_kernel(Args A) {
         a = __dadd_rn(a, __dmul_rn(scale, g1));
         g1 = g2;
         sz = sz1;
-        gp++;
-        sp++;
-        g2 = __ldg(gp + 1);
-        sz1 = __ldg(sp + 1);
+        if (IL4) {
+            g2 = __ldg(gap + il4_off(j + 3));
+            sz1 = __ldg(gap + il4_off(n + j + 2));
+        } else {
+            gp++;
+            sp++;
+            g2 = __ldg(gp + 1);
+            sz1 = __ldg(sp + 1);
+        }
         j++;
         // per-job sums over the windows (interval [a, f) in system, [st, f)
         // in service, clipped to [w_start, T]); jobs that end past the
@@ -686,14 +716,14 @@ struct Plan {
 
 static int pick_cmax(int32_t max_cap) { return max_cap <= 4 ? 4 : max_cap <= 7 ? 7 : max_cap <= 8 ? 8 : 16; }
 
-template <int CMAX>
+template <int CMAX, bool IL4>
 static int max_resident_blocks() {
     static int cached[64] = {0};
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return 0;
     if (dev < 64 && cached[dev]) return cached[dev];
     int per_sm = 0, sms = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jffc_seg_kernel<CMAX>, 32, 0) != cudaSuccess ||
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jffc_seg_kernel<CMAX, IL4>, 32, 0) != cudaSuccess ||
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
         cudaGetLastError();
         return 0;
@@ -705,10 +735,10 @@ static int max_resident_blocks() {
 
 static int resident_blocks(int cmax) {
     switch (cmax) {
-        case 4: return max_resident_blocks<4>();
-        case 7: return max_resident_blocks<7>();
-        case 8: return max_resident_blocks<8>();
-        default: return max_resident_blocks<16>();
+        case 4: return std::min(max_resident_blocks<4, false>(), max_resident_blocks<4, true>());
+        case 7: return std::min(max_resident_blocks<7, false>(), max_resident_blocks<7, true>());
+        case 8: return std::min(max_resident_blocks<8, false>(), max_resident_blocks<8, true>());
+        default: return std::min(max_resident_blocks<16, false>(), max_resident_blocks<16, true>());
     }
 }
 
@@ -750,7 +780,7 @@ static Plan make_plan(int32_t P, int32_t R, int32_t max_cap, int64_t n) {
     return pl;
 }
 
-template <int CMAX>
+template <int CMAX, bool IL4>
 static int launch(const Plan& pl, Args A, cudaStream_t st) {
     const int blocks = pl.S * pl.G;
     const bool trace = getenv("CS_SEG_TRACE") != nullptr;  // development timeline (stderr)
@@ -764,10 +794,10 @@ static int launch(const Plan& pl, Args A, cudaStream_t st) {
     if (pl.S > 1) {  // phase-2 waits need every segment resident
         void* params[] = {&A};
         const cudaError_t e =
-            cudaLaunchCooperativeKernel((const void*)jffc_seg_kernel<CMAX>, dim3(blocks), dim3(32), params, 0, st);
+            cudaLaunchCooperativeKernel((const void*)jffc_seg_kernel<CMAX, IL4>, dim3(blocks), dim3(32), params, 0, st);
         if (e != cudaSuccess) return check_cuda(e, "jffc_seg_kernel (cooperative launch)");
     } else {
-        jffc_seg_kernel<CMAX><<<blocks, 32, 0, st>>>(A);
+        jffc_seg_kernel<CMAX, IL4><<<blocks, 32, 0, st>>>(A);
     }
     int rc = check_launch("jffc_seg_kernel");
     if (rc) return rc;
@@ -860,7 +890,7 @@ extern "C" int cs_seg_sim_impl(const cs_sim_point* d_points, int32_t P, const do
                                const int32_t* d_caps, int32_t max_cap, const double* d_streams,
                                int64_t lds, int32_t rb, int32_t R, int32_t RT, int64_t n, int64_t warm,
                                double* d_resp, int64_t ldr, double* d_busy, int32_t ldb,
-                               cs_rep_summary* d_summ, void* d_ws, int64_t ws_bytes, int prefix_ready,
+                               cs_rep_summary* d_summ, void* d_ws, int64_t ws_bytes, int32_t flags,
                                void* stream) {
     using namespace cs;
     using namespace cs::seg;
@@ -872,7 +902,9 @@ extern "C" int cs_seg_sim_impl(const cs_sim_point* d_points, int32_t P, const do
     }
     cudaStream_t st = (cudaStream_t)stream;
     char* ws = (char*)d_ws;
+    const bool prefix_ready = flags & CS_SIM_PREFIX_READY;
     Args A{};
+    A.il4 = (flags & CS_SIM_STREAMS_IL4) ? 1 : 0;
     A.pts = d_points;
     A.rates = d_rates;
     A.caps = d_caps;
@@ -930,9 +962,9 @@ extern "C" int cs_seg_sim_impl(const cs_sim_point* d_points, int32_t P, const do
         cudaEventDestroy(ev1);
     }
     switch (pl.cmax) {
-        case 4: return launch<4>(pl, A, st);
-        case 7: return launch<7>(pl, A, st);
-        case 8: return launch<8>(pl, A, st);
-        default: return launch<16>(pl, A, st);
+        case 4: return A.il4 ? launch<4, true>(pl, A, st) : launch<4, false>(pl, A, st);
+        case 7: return A.il4 ? launch<7, true>(pl, A, st) : launch<7, false>(pl, A, st);
+        case 8: return A.il4 ? launch<8, true>(pl, A, st) : launch<8, false>(pl, A, st);
+        default: return A.il4 ? launch<16, true>(pl, A, st) : launch<16, false>(pl, A, st);
     }
 }

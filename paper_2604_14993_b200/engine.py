@@ -100,7 +100,7 @@ class SweepEngine:
                 "summ": torch.empty(self.P * self.R * C.sizeof(N.RepSummary), dtype=torch.uint8,
                                     device=dev),
                 "ws": torch.empty(max(self.ws_bytes, 16), dtype=torch.uint8, device=dev),
-                "ready": C.c_int32(0)}
+                "flags": C.c_int32(0)}  # simulation flags cs_sim_streams returns
 
     # -- stages (buffer set b, CUDA stream st) ------------------------------
     def streams(self, b: int = 0, st=None):
@@ -109,7 +109,7 @@ class SweepEngine:
         rc = self.lib.cs_sim_streams(self.d_keys.data_ptr(), self.R, self.lds, B["S"].data_ptr(), self.lds,
                                      self.log1p_variant, self.d_pts.data_ptr(), self.P, self.max_chains,
                                      self.max_cap, self.n, self.warm, B["ws"].data_ptr(), self.ws_bytes,
-                                     C.byref(B["ready"]), st.cuda_stream)
+                                     C.byref(B["flags"]), st.cuda_stream)
         N.check(rc, "cs_sim_streams")
 
     def simulate(self, b: int = 0, st=None):
@@ -120,7 +120,7 @@ class SweepEngine:
             self.max_chains, self.max_cap, B["S"].data_ptr(), self.lds, 0, self.R, self.R, self.n,
             self.warm, B["resp"].data_ptr(), self.ldr, B["busy"].data_ptr(), self.ldb,
             B["summ"].data_ptr(), None, B["ws"].data_ptr(), self.ws_bytes,
-            N.CS_SIM_PREFIX_READY if B["ready"].value else 0, st.cuda_stream)
+            B["flags"].value, st.cuda_stream)
         N.check(rc, "cs_jffc_sim_ex")
 
     def statistics(self, b: int = 0, st=None):

@@ -146,9 +146,36 @@ def test_engine_fused_prefix_equals_host_path(eng):
     e = SweepEngine([system.rates] * 3, [system.capacities] * 3, lams, n, 0.1, 2, R)
     e.step()
     torch.cuda.synchronize()
-    assert e.sets[0]["ready"].value == 1
+    assert e.sets[0]["flags"].value & 1  # CS_SIM_PREFIX_READY
     res = eng.simulate_sweep([system.rates] * 3, [system.capacities] * 3, lams, n, 0.1, 2, R)
     got = e.summaries(0)
     for f in ("wait_sum", "service_sum", "mean_occupancy", "end_queue_len", "window_s", "resp_mean"):
         assert np.array_equal(np.asarray(got[f]).view(np.uint64), np.asarray(res.summaries[f]).view(np.uint64)), f
     assert e.order_stats() == res.order_stats
+
+
+@pytest.mark.parametrize("R", [64, 40], ids=["interleaved", "row_major"])
+def test_stream_layouts_vs_oracle(eng, oracle, R):
+    """Few points per stream: the streams are written in the simulator's
+    32-row interleaved layout when the replication count is a multiple of 32
+    (CS_SIM_STREAMS_IL4), row-major otherwise; both exact against the oracle."""
+    import torch
+
+    from paper_2604_14993_b200 import _native as N
+    from paper_2604_14993_b200.engine import SweepEngine
+
+    system = _petals(eng)
+    lams = [system.total_rate * x for x in (0.5, 0.93)]
+    n = 20_000
+    e = SweepEngine([system.rates] * 2, [system.capacities] * 2, lams, n, 0.1, 4, R)
+    e.step()
+    torch.cuda.synchronize()
+    il4 = bool(e.sets[0]["flags"].value & N.CS_SIM_STREAMS_IL4)
+    assert il4 == (R % 32 == 0)
+    res = eng.simulate_sweep([system.rates] * 2, [system.capacities] * 2, lams, n, 0.1, 4, R,
+                             return_responses=True)
+    for p in range(2):
+        _check_rows(res, p, oracle, system.rates, system.capacities, lams[p], n, 0.1, 4, R)
+    got = e.summaries(0)
+    for f in ("wait_sum", "mean_occupancy", "end_queue_len", "resp_mean"):
+        assert np.array_equal(np.asarray(got[f]).view(np.uint64), np.asarray(res.summaries[f]).view(np.uint64)), f
