@@ -464,7 +464,9 @@ def main():
     }
     if prof is not None:
         k = prof["kernels"]
-        sim_k = [x for x in ("seg_prefix_kernel", "jffc_seg_kernel", "seg_finalize_kernel") if x in k]
+        # kernel names carry their template arguments (jffc_seg_kernel<7, false>)
+        sim_k = [x for x in k if any(x.split("<")[0].endswith(base) for base in
+                                     ("seg_prefix_kernel", "jffc_seg_kernel", "seg_finalize_kernel"))]
         sim_inst = sum(k[x]["inst_executed"] for x in sim_k)
         roof["achieved"] = sim_inst / (sim_ms / 1e3)
         roof["frac"] = roof["achieved"] / issue_peak

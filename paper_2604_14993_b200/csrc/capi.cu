@@ -380,8 +380,14 @@ int cs_run_sim_host(const cs_sim_point* points, int32_t n_points, const double* 
     const int64_t rows = (int64_t)n_points * n_reps;
     // replications per stream chunk (bounded stream scratch)
     int64_t chunk = n_reps;
-    if (max_stream_bytes > 0)
-        chunk = std::max<int64_t>(1, std::min<int64_t>(n_reps, max_stream_bytes / (lds * 8)));
+    if (max_stream_bytes > 0) {
+        const int64_t cmax = std::max<int64_t>(1, std::min<int64_t>(n_reps, max_stream_bytes / (lds * 8)));
+        // equal chunks, multiples of 32 where possible (the simulator's
+        // interleaved stream layout needs whole 32-row groups)
+        const int64_t nch = (n_reps + cmax - 1) / cmax;
+        chunk = (n_reps + nch - 1) / nch;
+        if (nch > 1 && cmax >= 32) chunk = std::min(cmax / 32 * 32, (chunk + 31) / 32 * 32);
+    }
     DevBuf b_pts, b_rates, b_caps, b_keys, b_S, b_resp, b_busy, b_summ, b_jobs, b_ws;
     if ((rc = b_pts.alloc(sizeof(cs_sim_point) * n_points, st)) ||
         (rc = b_rates.alloc(sizeof(double) * n_chain_entries, st)) ||

@@ -73,9 +73,16 @@ __global__ void __launch_bounds__(EXP_WARPS * 32) exp_streams_kernel(const uint6
     int entry = 0;            // warp-uniform: offset of the first attempt in this chunk
     uint64_t pend_w = 0;      // word that started the carried slow attempt (entry == 1)
     uint64_t chunk = 0;
+    // software-pipelined: the next chunk's Philox blocks (a long dependent
+    // multiply chain per lane) are computed while this chunk is classified,
+    // scanned, emitted and summed
+    uint64_t wn[4];
+    philox4x64_10(lane + 1, 0, 0, 0, k0, k1, wn);
     while (produced < n_draws) {
         uint64_t w[4];
-        philox4x64_10(chunk * 32 + lane + 1, 0, 0, 0, k0, k1, w);
+#pragma unroll
+        for (int q = 0; q < 4; q++) w[q] = wn[q];
+        philox4x64_10((chunk + 1) * 32 + lane + 1, 0, 0, 0, k0, k1, wn);
         const uint64_t wnext = __shfl_down_sync(0xffffffffu, w[0], 1);
 
         // Per-word attempt results.

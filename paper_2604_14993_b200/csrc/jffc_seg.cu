@@ -122,6 +122,20 @@ __device__ __forceinline__ int32_t ld_acquire(const int32_t* p) {
     asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+// Spin-wait polls are relaxed (L2, no L1 invalidation: an acquire load
+// invalidates the SM's whole L1, i.e. the stream lines the other warps on
+// the SM are reading); one acquire fence follows the successful poll.
+__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ int32_t ld_relaxed(const int32_t* p) {
+    int32_t v;
+    asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void fence_acquire() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 __device__ __forceinline__ void st_release(int32_t* p, int32_t v) {
     asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -597,9 +611,10 @@ __global__ void __launch_bounds__(32, CS_SEG_MINB) jffc_seg_kernel(Args A) {
     if (s > 0) {
         int32_t stv = valid ? ST_UNKNOWN : ST_SKIPPED;
         while (__any_sync(FULL, stv == ST_UNKNOWN)) {
-            if (stv == ST_UNKNOWN) stv = ld_acquire(A.status + (int64_t)s * T + tid);
+            if (stv == ST_UNKNOWN) stv = ld_relaxed(A.status + (int64_t)s * T + tid);
             if (__any_sync(FULL, stv == ST_UNKNOWN)) __nanosleep(256);
         }
+        fence_acquire();
         act = valid && stv >= 2;
     }
     if (tr && lane == 0) tr[2] = gtimer();
@@ -608,7 +623,8 @@ __global__ void __launch_bounds__(32, CS_SEG_MINB) jffc_seg_kernel(Args A) {
         // entering segment t's range: its phase-1 writes (responses, blocks)
         // must be complete before ours overwrite them
         const uint32_t* prog = A.progress + (int64_t)t * G + g;
-        while (!(ld_acquire(prog) & DONE)) __nanosleep(256);
+        while (!(ld_relaxed(prog) & DONE)) __nanosleep(256);
+        fence_acquire();
         const int64_t bt = seg_begin(t, S, n), et = seg_begin(t + 1, S, n);
         const double* tcf = A.ckf + (((int64_t)t * G + g) * Q) * FCK * 32 + lane;
         const uint32_t* tck = A.ckk + (((int64_t)t * G + g) * Q) * CMAX * 32 + lane;
