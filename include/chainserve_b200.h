@@ -47,6 +47,12 @@ int cs_host_log1p_variant(void);
 int cs_device_count(void);
 /* kernels launched by this library since load (all threads) */
 int64_t cs_launch_count(void);
+/* The host-level calls (cs_run_sim_host, cs_rep_stats*) take their device
+ * scratch from a private stream-ordered pool that keeps freed memory reserved
+ * for the next call (re-mapping tens of GB per call costs more than the
+ * simulation).  This returns the current device's unused reserve to the
+ * driver; it blocks until the device is idle. */
+int cs_release_memory(void);
 
 /* ------------------------------------------------------------------------ */
 /* RNG                                                                        */

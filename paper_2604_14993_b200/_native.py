@@ -68,6 +68,7 @@ assert SUMMARY_DTYPE.itemsize == C.sizeof(RepSummary)
 
 EXPORTS = (
     "cs_version", "cs_last_error", "cs_host_log1p_variant", "cs_device_count", "cs_launch_count",
+    "cs_release_memory",
     "cs_philox_keys", "cs_exp_streams", "cs_jffc_sim", "cs_jffc_sim_workspace_bytes", "cs_seg_plan", "cs_philox_peak", "cs_sim_streams", "cs_jffc_sim_ex",
     "cs_rep_stats", "cs_rep_stats_dist", "cs_run_sim_host", "cs_gbp_batch", "cs_gca_batch",
     "cs_nccl_unique_id", "cs_comm_init", "cs_comm_destroy", "cs_occupancy_bounds",

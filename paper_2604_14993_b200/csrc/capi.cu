@@ -51,10 +51,10 @@ static std::atomic<long long> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 // The engine's own stream-ordered pool per device (not the device's default
-// pool, which other libraries share): up to 4 GiB of freed scratch stays
-// reserved across calls (the statistics' small per-call buffers), anything
-// beyond is returned to the driver at the next synchronisation (the
-// multi-GB response / stream buffers of cs_run_sim_host).
+// pool, which other libraries share).  Freed scratch stays reserved: with a
+// release threshold the driver trims the pool at every synchronisation and
+// the next allocation re-maps it (measured 18-40 ms per multi-GB buffer, more
+// than a whole config-2 sweep); cs_release_memory() trims on request.
 static cudaMemPool_t g_pools[64] = {};
 
 void ensure_mem_pool() { (void)engine_pool(); }
@@ -74,7 +74,7 @@ cudaMemPool_t engine_pool() {
             g_pools[dev] = nullptr;
             return nullptr;
         }
-        uint64_t thr = 4ull << 30;
+        uint64_t thr = ~0ull;
         cudaMemPoolSetAttribute(g_pools[dev], cudaMemPoolAttrReleaseThreshold, &thr);
     }
     return g_pools[dev];
@@ -143,6 +143,14 @@ int cs_host_log1p_variant(void) {
 #else
     return 0;
 #endif
+}
+
+int cs_release_memory(void) {
+    cudaMemPool_t pool = engine_pool();
+    if (!pool) return CS_OK;
+    int rc = check_cuda(cudaDeviceSynchronize(), "cs_release_memory sync");
+    if (rc) return rc;
+    return check_cuda(cudaMemPoolTrimTo(pool, 0), "cudaMemPoolTrimTo");
 }
 
 int cs_device_count(void) {

@@ -381,6 +381,12 @@ def simulate_sweep(rates_list: Sequence[Sequence[float]], caps_list: Sequence[Se
                        resp.reshape(P, R, m) if resp is not None else None)
 
 
+def release_memory() -> None:
+    """Return the engine's reserved device scratch (kept across calls: the
+    host-buffer path re-uses it instead of re-mapping tens of GB per call)."""
+    N.check(N.load().cs_release_memory(), "cs_release_memory")
+
+
 def run_sim_batch(configs: Sequence[SimConfig]) -> list[SimStats]:
     """Batched run_sim: configs that differ only in rates/capacities/arrival
     rate share one GPU call (and their common random number streams)."""
