@@ -27,55 +27,21 @@ struct Xfer {
     int c0, c1;  // values emitted for entry 0 / 1
 };
 
-// Fused arrival-time prefix (the segmented simulator's pre-pass, see
-// jffc_seg.cu): while the first n_cum draws of stream r are generated, lane p
-// of its warp (p < P, the sweep points sharing the stream) runs the exact
-// sequential cumsum a_j = a_{j-1} + (1/lam_p) * S_j of np.cumsum and records
-// a_j at the listed job indices into out[(r * P + p) * ncol + col].
-// streams (warps) per block; each warp's chunk loop is latency-bound, so the
-// block shape barely matters (4 per block measured 2% slower than 8)
-constexpr int EXP_WARPS = 8;
-
-// IL4 (with PFX only): the output in the simulator's interleaved layout
-// (jffc_seg.cu il4_off): stream r's value i at (r / 32) * 32 * ld +
-// (i / 4) * 128 + (r % 32) * 4 + i % 4, written from the chunk buffer.
-template <bool PFX, bool IL4>
-__global__ void __launch_bounds__(EXP_WARPS * 32) exp_streams_kernel(const uint64_t* __restrict__ keys,
-                                                          int64_t n_streams, int64_t n_draws,
-                                                          double* __restrict__ out, int64_t ld,
-                                                          int log1p_fma,
-                                                          int64_t* __restrict__ words_used,
-                                                          const PrefixPlan pp) {
-    __shared__ ZigSmem zs;
-    __shared__ double sh_vals[PFX ? EXP_WARPS : 1][136];  // a chunk's values (<= 128 + carry), per warp
-    zig_load(&zs);
-    __syncthreads();
-    const int lane = threadIdx.x & 31;
-    const int64_t stream = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (stream >= n_streams) return;
-    const uint64_t k0 = keys[2 * stream], k1 = keys[2 * stream + 1];
-    double* __restrict__ o = IL4 ? out + (stream >> 5) * 32 * ld + (stream & 31) * 4 : out + stream * ld;
-    double* cv = sh_vals[PFX ? (threadIdx.x >> 5) : 0];
-    // prefix state: lane p handles point p (P <= 32 per pass; more points loop)
-    double pa[PFX ? PrefixPlan::MAXP32 : 1];
-    double pscale[PFX ? PrefixPlan::MAXP32 : 1];
-    int ev = 0;  // next event of the (uniform) event list
-    if (PFX) {
-#pragma unroll
-        for (int g = 0; g < PrefixPlan::MAXP32; g++) {
-            const int p = g * 32 + lane;
-            pscale[g] = p < pp.P ? __ddiv_rn(1.0, pp.pts[p].lam) : 0.0;
-            pa[g] = 0.0;
-        }
-    }
-
+// The generator loop of one stream (one warp).  For every chunk, emit(i, v)
+// is called by the lanes holding values (i = index within the chunk, in
+// stream order) and then chunk_done(produced, tot) by every lane (produced =
+// the stream's values before this chunk, tot = this chunk's count; emitted
+// values may run past n_draws, the callbacks clip).
+template <typename Emit, typename Done>
+__device__ __forceinline__ int64_t gen_stream(const ZigSmem* zs, int lane, uint64_t k0, uint64_t k1,
+                                              int64_t n_draws, int log1p_fma, Emit&& emit, Done&& chunk_done) {
     int64_t produced = 0;
-    int entry = 0;            // warp-uniform: offset of the first attempt in this chunk
-    uint64_t pend_w = 0;      // word that started the carried slow attempt (entry == 1)
+    int entry = 0;        // warp-uniform: offset of the first attempt in this chunk
+    uint64_t pend_w = 0;  // word that started the carried slow attempt (entry == 1)
     uint64_t chunk = 0;
     // software-pipelined: the next chunk's Philox blocks (a long dependent
     // multiply chain per lane) are computed while this chunk is classified,
-    // scanned, emitted and summed
+    // scanned and emitted
     uint64_t wn[4];
     philox4x64_10(lane + 1, 0, 0, 0, k0, k1, wn);
     while (produced < n_draws) {
@@ -92,12 +58,12 @@ __global__ void __launch_bounds__(EXP_WARPS * 32) exp_streams_kernel(const uint6
 #pragma unroll
         for (int p = 0; p < 4; p++) {
             double x;
-            if (zig_fast(&zs, w[p], &x)) {
+            if (zig_fast(zs, w[p], &x)) {
                 v[p] = x;
                 adv[p] = 1;
                 has[p] = true;
             } else if (p < 3 || lane < 31) {
-                const ZigAttempt a = zig_slow(&zs, w[p], p < 3 ? w[p + 1] : wnext, log1p_fma);
+                const ZigAttempt a = zig_slow(zs, w[p], p < 3 ? w[p + 1] : wnext, log1p_fma);
                 v[p] = a.v;
                 adv[p] = 2;
                 has[p] = a.has;
@@ -111,7 +77,7 @@ __global__ void __launch_bounds__(EXP_WARPS * 32) exp_streams_kernel(const uint6
         bool carry_has = false;
         double carry_v = 0.0;
         if (lane == 0 && entry == 1) {
-            const ZigAttempt a = zig_slow(&zs, pend_w, w[0], log1p_fma);
+            const ZigAttempt a = zig_slow(zs, pend_w, w[0], log1p_fma);
             carry_has = a.has;
             carry_v = a.v;
         }
@@ -164,22 +130,13 @@ __global__ void __launch_bounds__(EXP_WARPS * 32) exp_streams_kernel(const uint6
         int pos = lane == 0 ? 0 : (entry ? ex_c1 : ex_c0);
 
         // Emit this lane's values.
-        int64_t base = produced + pos;
-        if (carry_has) {
-            if (!IL4 && base < n_draws) o[base] = carry_v;
-            if (PFX) cv[base - produced] = carry_v;
-            base++;
-        }
+        if (carry_has) emit(pos++, carry_v);
         {
             int p = my_entry;
 #pragma unroll
             for (int q = 0; q < 4; q++)
                 if (p == q) {
-                    if (has[q]) {
-                        if (!IL4 && base < n_draws) o[base] = v[q];
-                        if (PFX) cv[base - produced] = v[q];
-                        base++;
-                    }
+                    if (has[q]) emit(pos++, v[q]);
                     p += adv[q];
                 }
         }
@@ -187,58 +144,118 @@ __global__ void __launch_bounds__(EXP_WARPS * 32) exp_streams_kernel(const uint6
         const int tot = __shfl_sync(0xffffffffu, entry ? inc.c1 : inc.c0, 31);
         const int nxt = __shfl_sync(0xffffffffu, entry ? inc.x1 : inc.x0, 31);
         pend_w = __shfl_sync(0xffffffffu, w[3], 31);
-        if (IL4) {  // the chunk's values in order: 4-value sectors of this row
-            __syncwarp();
-            for (int i = lane; i < tot; i += 32) {
-                const int64_t q = produced + i;
-                if (q < n_draws) o[((q >> 2) << 7) + (q & 3)] = cv[i];
-            }
-        }
-        if (PFX && produced < pp.n_cum) {
-            __syncwarp();
-            const int cnt = (int)min((int64_t)tot, pp.n_cum - produced);
-            const int32_t j0 = (int32_t)produced;
-#pragma unroll
-            for (int g = 0; g < PrefixPlan::MAXP32; g++) {
-                const int p = g * 32 + lane;
-                if (g * 32 >= pp.P) break;
-                double a = pa[g];
-                const double sc = pscale[g];
-                int e = ev;
-                if (j0 > 0 && (e >= pp.nev || pp.ev_idx[e] >= j0 + cnt)) {  // no event in the chunk
-                    int i = 0;
-                    for (; i + 4 <= cnt; i += 4) {
-                        a = __dadd_rn(a, __dmul_rn(sc, cv[i]));
-                        a = __dadd_rn(a, __dmul_rn(sc, cv[i + 1]));
-                        a = __dadd_rn(a, __dmul_rn(sc, cv[i + 2]));
-                        a = __dadd_rn(a, __dmul_rn(sc, cv[i + 3]));
-                    }
-                    for (; i < cnt; i++) a = __dadd_rn(a, __dmul_rn(sc, cv[i]));
-                } else {
-                    for (int i = 0; i < cnt; i++) {
-                        const double x = __dmul_rn(sc, cv[i]);
-                        const int32_t j = j0 + i;
-                        a = j == 0 ? x : __dadd_rn(a, x);
-                        while (e < pp.nev && pp.ev_idx[e] == j) {
-                            if (p < pp.P) pp.out[((int64_t)stream * pp.P + p) * pp.ncol + pp.ev_col[e]] = a;
-                            e++;
-                        }
-                    }
-                }
-                pa[g] = a;
-                ev = e;
-            }
-            __syncwarp();
-        }
+        chunk_done(produced, tot);
         produced += tot;
         entry = nxt;
         chunk++;
     }
-    if (words_used != nullptr && lane == 0) {
-        // Exact word count only when the stream ended on a chunk boundary is not
-        // needed by the simulator; report the chunk-granular upper bound.
-        words_used[stream] = (int64_t)(chunk * 128);
-    }
+    return (int64_t)chunk;
+}
+
+// streams (warps) per block; each warp's chunk loop is latency-bound, so the
+// block shape barely matters (4 per block measured 2% slower than 8)
+constexpr int EXP_WARPS = 8;
+
+__global__ void __launch_bounds__(EXP_WARPS * 32) exp_streams_kernel(const uint64_t* __restrict__ keys,
+                                                                     int64_t n_streams, int64_t n_draws,
+                                                                     double* __restrict__ out, int64_t ld,
+                                                                     int log1p_fma) {
+    __shared__ ZigSmem zs;
+    zig_load(&zs);
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int64_t stream = (int64_t)blockIdx.x * EXP_WARPS + (threadIdx.x >> 5);
+    if (stream >= n_streams) return;
+    double* __restrict__ o = out + stream * ld;
+    int64_t base = 0;
+    gen_stream(
+        &zs, lane, keys[2 * stream], keys[2 * stream + 1], n_draws, log1p_fma,
+        [&](int i, double x) {
+            if (base + i < n_draws) o[base + i] = x;
+        },
+        [&](int64_t produced, int tot) { base = produced + tot; });
+}
+
+// Streams plus the segmented simulator's arrival-time prefix (jffc_seg.cu):
+// while the first n_cum draws of stream r are generated, lane p of its warp
+// (p < P, the sweep points sharing the stream) runs the exact sequential
+// cumsum a_j = a_{j-1} + (1/lam_p) * S_j of np.cumsum over each chunk's values
+// (in shared memory) and records a_j at the listed job indices into
+// out[(r * P + p) * ncol + col].
+// (Measured against a split design -- producer warps handing chunks to
+// separate prefix warps through a shared-memory ring -- which lost: the
+// prefix lanes of one warp serve several streams in lockstep and stall the
+// producers, 3.9 -> 5.9 ms on config 2, 56 -> 192 ms per 2048 config-5 streams.)
+//
+// IL4: the output in the simulator's interleaved layout (jffc_seg.cu il4_off):
+// stream r's value i at (r / 32) * 32 * ld + (i / 4) * 128 + (r % 32) * 4 + i % 4,
+// written from the chunk buffer in order.
+__device__ __forceinline__ int64_t il4_pos(int64_t i) { return ((i >> 2) << 7) + (i & 3); }
+
+template <bool IL4>
+__global__ void __launch_bounds__(EXP_WARPS * 32) exp_streams_prefix_kernel(
+    const uint64_t* __restrict__ keys, int64_t n_streams, int64_t n_draws, double* __restrict__ out,
+    int64_t ld, int log1p_fma, const PrefixPlan pp) {
+    __shared__ ZigSmem zs;
+    __shared__ double sh_vals[EXP_WARPS][136];  // a chunk's values (<= 128 + carry), per warp
+    zig_load(&zs);
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t stream = (int64_t)blockIdx.x * EXP_WARPS + warp;
+    if (stream >= n_streams) return;
+    double* __restrict__ o = IL4 ? out + (stream >> 5) * 32 * ld + (stream & 31) * 4 : out + stream * ld;
+    double* cv = sh_vals[warp];
+    // lane p < P: point p's chain (P <= 32)
+    const bool pl = lane < pp.P;
+    const double sc = pl ? __ddiv_rn(1.0, pp.pts[lane].lam) : 0.0;
+    double* rec = pl ? pp.out + (stream * pp.P + lane) * pp.ncol : nullptr;
+    double a = 0.0;
+    int ev = 0;  // next event of the (uniform) event list
+    int64_t base = 0;
+    gen_stream(
+        &zs, lane, keys[2 * stream], keys[2 * stream + 1], n_draws, log1p_fma,
+        [&](int i, double x) {
+            cv[i] = x;
+            if (!IL4 && base + i < n_draws) o[base + i] = x;
+        },
+        [&](int64_t produced, int tot) {
+            __syncwarp();
+            if (IL4) {  // the chunk's values in order: 4-value sectors of this row
+                for (int i = lane; i < tot; i += 32) {
+                    const int64_t q = produced + i;
+                    if (q < n_draws) o[il4_pos(q)] = cv[i];
+                }
+            }
+            if (produced < pp.n_cum) {
+                const int cnt = (int)min((int64_t)tot, pp.n_cum - produced);
+                const int32_t j0 = (int32_t)produced;
+                if (pl) {
+                    if (j0 > 0 && (ev >= pp.nev || pp.ev_idx[ev] >= j0 + cnt)) {  // no event in the chunk
+                        int i = 0;
+                        for (; i + 4 <= cnt; i += 4) {
+                            a = __dadd_rn(a, __dmul_rn(sc, cv[i]));
+                            a = __dadd_rn(a, __dmul_rn(sc, cv[i + 1]));
+                            a = __dadd_rn(a, __dmul_rn(sc, cv[i + 2]));
+                            a = __dadd_rn(a, __dmul_rn(sc, cv[i + 3]));
+                        }
+                        for (; i < cnt; i++) a = __dadd_rn(a, __dmul_rn(sc, cv[i]));
+                    } else {
+                        for (int i = 0; i < cnt; i++) {
+                            const double x = __dmul_rn(sc, cv[i]);
+                            const int32_t j = j0 + i;
+                            a = j == 0 ? x : __dadd_rn(a, x);
+                            while (ev < pp.nev && pp.ev_idx[ev] == j) {
+                                rec[pp.ev_col[ev]] = a;
+                                ev++;
+                            }
+                        }
+                    }
+                }
+                ev = __shfl_sync(0xffffffffu, ev, 0);  // lanes >= P track the event list too
+            }
+            base = produced + tot;
+            __syncwarp();  // cv is rewritten by the next chunk
+        });
 }
 
 // Measurement kernel (no reference counterpart): Philox4x64-10 blocks as
@@ -269,11 +286,9 @@ extern "C" int cs_philox_peak_impl(int64_t blocks_per_thread, int32_t grid, uint
 extern "C" int cs_exp_streams_impl(const uint64_t* d_keys, int64_t n_streams, int64_t n_draws,
                                    double* d_out, int64_t ld, int log1p_fma, void* stream) {
     if (n_streams <= 0 || n_draws <= 0) return 0;
-    const int warps_per_block = cs::EXP_WARPS;
-    const int64_t blocks = (n_streams + warps_per_block - 1) / warps_per_block;
-    cs::PrefixPlan none{};
-    cs::exp_streams_kernel<false, false><<<(unsigned)blocks, warps_per_block * 32, 0, (cudaStream_t)stream>>>(
-        d_keys, n_streams, n_draws, d_out, ld, log1p_fma, nullptr, none);
+    const int64_t blocks = (n_streams + cs::EXP_WARPS - 1) / cs::EXP_WARPS;
+    cs::exp_streams_kernel<<<(unsigned)blocks, cs::EXP_WARPS * 32, 0, (cudaStream_t)stream>>>(
+        d_keys, n_streams, n_draws, d_out, ld, log1p_fma);
     return cs::check_launch("exp_streams_kernel");
 }
 
@@ -282,13 +297,13 @@ extern "C" int cs_exp_streams_prefix_impl(const uint64_t* d_keys, int64_t n_stre
                                           double* d_out, int64_t ld, int log1p_fma,
                                           const cs::PrefixPlan* plan, int il4, void* stream) {
     if (n_streams <= 0 || n_draws <= 0) return 0;
-    const int warps_per_block = cs::EXP_WARPS;
-    const int64_t blocks = (n_streams + warps_per_block - 1) / warps_per_block;
+    const int64_t blocks = (n_streams + cs::EXP_WARPS - 1) / cs::EXP_WARPS;
+    cudaStream_t st = (cudaStream_t)stream;
     if (il4)
-        cs::exp_streams_kernel<true, true><<<(unsigned)blocks, warps_per_block * 32, 0, (cudaStream_t)stream>>>(
-            d_keys, n_streams, n_draws, d_out, ld, log1p_fma, nullptr, *plan);
+        cs::exp_streams_prefix_kernel<true><<<(unsigned)blocks, cs::EXP_WARPS * 32, 0, st>>>(
+            d_keys, n_streams, n_draws, d_out, ld, log1p_fma, *plan);
     else
-        cs::exp_streams_kernel<true, false><<<(unsigned)blocks, warps_per_block * 32, 0, (cudaStream_t)stream>>>(
-            d_keys, n_streams, n_draws, d_out, ld, log1p_fma, nullptr, *plan);
-    return cs::check_launch("exp_streams_kernel<prefix>");
+        cs::exp_streams_prefix_kernel<false><<<(unsigned)blocks, cs::EXP_WARPS * 32, 0, st>>>(
+            d_keys, n_streams, n_draws, d_out, ld, log1p_fma, *plan);
+    return cs::check_launch("exp_streams_prefix_kernel");
 }
