@@ -407,7 +407,7 @@ def main():
     # warm-up, then K complete sweeps pipelined over two buffer sets: each
     # simulation runs alone (its kernel fills every SM), the statistics of
     # sweep k overlap the streams of sweep k+1
-    eng.run_pipelined(max(args.warmup, 3), gather, ordered=True)
+    eng.run_pipelined(max(args.warmup, 3), gather)
     barrier()
     launches0 = eng.lib.cs_launch_count()
     with ClockSampler(local) as clk:
@@ -415,7 +415,7 @@ def main():
         t_end = torch.cuda.Event(enable_timing=True)
         barrier()
         t_start.record()
-        eng.run_pipelined(args.steps, gather, ordered=True)
+        eng.run_pipelined(args.steps, gather)
         t_end.record()
         barrier()
     ms = t_start.elapsed_time(t_end)

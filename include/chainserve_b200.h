@@ -156,6 +156,18 @@ int cs_sim_streams(const uint64_t* d_keys, int64_t n_streams, int64_t n_draws, d
                    int32_t max_chains, int32_t max_capacity, int64_t n_jobs, int64_t warm,
                    void* d_workspace, int64_t workspace_bytes, int32_t* sim_flags, void* stream);
 
+/* cs_sim_streams with options.  CS_STREAMS_WHOLE_SM: the fused kernel runs
+ * 16 streams per block, each block filling one SM (ceil(n_streams / 16) SMs),
+ * for a caller that runs other work on the remaining SMs at the same time
+ * (the pipelined engine: the statistics of the previous sweep); alone on the
+ * GPU the default 8-stream blocks over every SM are faster. */
+#define CS_STREAMS_WHOLE_SM 1
+int cs_sim_streams_ex(const uint64_t* d_keys, int64_t n_streams, int64_t n_draws, double* d_out, int64_t ld,
+                      int32_t log1p_variant, const cs_sim_point* d_points, int32_t n_points,
+                      int32_t max_chains, int32_t max_capacity, int64_t n_jobs, int64_t warm,
+                      void* d_workspace, int64_t workspace_bytes, int32_t opts, int32_t* sim_flags,
+                      void* stream);
+
 /* cs_jffc_sim with flags (CS_SIM_PREFIX_READY: d_workspace holds the prefix
  * cs_sim_streams wrote for exactly these streams and shape; CS_SIM_STREAMS_IL4:
  * d_streams is in the interleaved layout; pass cs_sim_streams' *sim_flags). */

@@ -16,6 +16,7 @@ from .errors import InfeasibleError, UnstableError
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libchainserve_b200.so")
 
 CS_OK, CS_INFEASIBLE, CS_INVALID, CS_INTERNAL, CS_ERR_CUDA, CS_UNSUPPORTED, CS_UNSTABLE = range(7)
+CS_STREAMS_WHOLE_SM = 1
 CS_SIM_PREFIX_READY = 1
 CS_SIM_STREAMS_IL4 = 4
 CS_SIM_FORCE_EVENT_LOOP = 2
@@ -69,7 +70,7 @@ assert SUMMARY_DTYPE.itemsize == C.sizeof(RepSummary)
 EXPORTS = (
     "cs_version", "cs_last_error", "cs_host_log1p_variant", "cs_device_count", "cs_launch_count",
     "cs_release_memory",
-    "cs_philox_keys", "cs_exp_streams", "cs_jffc_sim", "cs_jffc_sim_workspace_bytes", "cs_seg_plan", "cs_philox_peak", "cs_sim_streams", "cs_jffc_sim_ex",
+    "cs_philox_keys", "cs_exp_streams", "cs_jffc_sim", "cs_jffc_sim_workspace_bytes", "cs_seg_plan", "cs_philox_peak", "cs_sim_streams", "cs_sim_streams_ex", "cs_jffc_sim_ex",
     "cs_rep_stats", "cs_rep_stats_dist", "cs_run_sim_host", "cs_gbp_batch", "cs_gca_batch",
     "cs_nccl_unique_id", "cs_comm_init", "cs_comm_destroy", "cs_occupancy_bounds",
     "cs_birth_death_occupancy", "cs_sim_ext", "cs_ragged_rows",
@@ -108,6 +109,7 @@ def load(require_device: bool = True):
         L.cs_sim_streams.argtypes = [vp, C.c_int64, C.c_int64, vp, C.c_int64, C.c_int32, vp, C.c_int32,
                                      C.c_int32, C.c_int32, C.c_int64, C.c_int64, vp, C.c_int64,
                                      P(C.c_int32), vp]
+        L.cs_sim_streams_ex.argtypes = L.cs_sim_streams.argtypes[:-2] + [C.c_int32, P(C.c_int32), vp]
         L.cs_rep_stats.argtypes = [vp, C.c_int32, C.c_int64, C.c_int64, C.c_int64, vp,
                                    P(C.c_int64), C.c_int32, P(C.c_double), vp, vp]
         L.cs_rep_stats_dist.argtypes = L.cs_rep_stats.argtypes

@@ -18,7 +18,7 @@ extern "C" int cs_jffc_sim_impl(const cs_sim_point*, int32_t, const double*, con
                                 int64_t, double*, int64_t, double*, int32_t, cs_rep_summary*, double*,
                                 void*, int64_t, int32_t, void*);
 extern "C" int cs_exp_streams_prefix_impl(const uint64_t*, int64_t, int64_t, double*, int64_t, int,
-                                          const cs::PrefixPlan*, int, void*);
+                                          const cs::PrefixPlan*, int, int, void*);
 extern "C" bool cs_seg_prefix_plan(int32_t, int32_t, int32_t, int64_t, int64_t, const cs_sim_point*, void*,
                                    cs::PrefixPlan*);
 namespace cs {
@@ -253,6 +253,15 @@ int cs_sim_streams(const uint64_t* d_keys, int64_t n_streams, int64_t n_draws, d
                    int32_t log1p_variant, const cs_sim_point* d_points, int32_t n_points,
                    int32_t max_chains, int32_t max_capacity, int64_t n_jobs, int64_t warm,
                    void* d_workspace, int64_t workspace_bytes, int32_t* sim_flags, void* stream) {
+    return cs_sim_streams_ex(d_keys, n_streams, n_draws, d_out, ld, log1p_variant, d_points, n_points, max_chains,
+                             max_capacity, n_jobs, warm, d_workspace, workspace_bytes, 0, sim_flags, stream);
+}
+
+int cs_sim_streams_ex(const uint64_t* d_keys, int64_t n_streams, int64_t n_draws, double* d_out, int64_t ld,
+                      int32_t log1p_variant, const cs_sim_point* d_points, int32_t n_points,
+                      int32_t max_chains, int32_t max_capacity, int64_t n_jobs, int64_t warm,
+                      void* d_workspace, int64_t workspace_bytes, int32_t opts, int32_t* sim_flags,
+                      void* stream) {
     if (sim_flags) *sim_flags = 0;
     if (cs_device_count() == 0) {
         set_error("cs_sim_streams: no CUDA device");
@@ -270,7 +279,8 @@ int cs_sim_streams(const uint64_t* d_keys, int64_t n_streams, int64_t n_draws, d
         cs_seg_prefix_plan(n_points, (int32_t)n_streams, max_capacity, n_jobs, warm, d_points, d_workspace, &pp)) {
         // few points per stream: every simulator lane reads its own row
         const bool il4 = n_points < 16 && n_streams % 32 == 0 && ld % 4 == 0;
-        const int rc = cs_exp_streams_prefix_impl(d_keys, n_streams, n_draws, d_out, ld, v, &pp, il4, stream);
+        const int rc = cs_exp_streams_prefix_impl(d_keys, n_streams, n_draws, d_out, ld, v, &pp, il4,
+                                                  (opts & CS_STREAMS_WHOLE_SM) ? 1 : 0, stream);
         if (rc == CS_OK) *sim_flags = CS_SIM_PREFIX_READY | (il4 ? CS_SIM_STREAMS_IL4 : 0);
         return rc;
     }

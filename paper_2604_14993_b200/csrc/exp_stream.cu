@@ -192,16 +192,20 @@ __global__ void __launch_bounds__(EXP_WARPS * 32) exp_streams_kernel(const uint6
 // written from the chunk buffer in order.
 __device__ __forceinline__ int64_t il4_pos(int64_t i) { return ((i >> 2) << 7) + (i & 3); }
 
-template <bool IL4>
-__global__ void __launch_bounds__(EXP_WARPS * 32) exp_streams_prefix_kernel(
+// W streams per block.  W = 16 (whole_sm): a block fills one SM's register
+// file, so the kernel occupies ceil(R / 16) whole SMs and leaves the others to
+// the statistics of the previous sweep running beside it (engine.py's
+// pipeline); alone on the GPU, 8-warp blocks spread over every SM are faster.
+template <bool IL4, int W>
+__global__ void __launch_bounds__(W * 32, W == 16 ? 1 : 2) exp_streams_prefix_kernel(
     const uint64_t* __restrict__ keys, int64_t n_streams, int64_t n_draws, double* __restrict__ out,
     int64_t ld, int log1p_fma, const PrefixPlan pp) {
     __shared__ ZigSmem zs;
-    __shared__ double sh_vals[EXP_WARPS][136];  // a chunk's values (<= 128 + carry), per warp
+    __shared__ double sh_vals[W][136];  // a chunk's values (<= 128 + carry), per warp
     zig_load(&zs);
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t stream = (int64_t)blockIdx.x * EXP_WARPS + warp;
+    const int64_t stream = (int64_t)blockIdx.x * W + warp;
     if (stream >= n_streams) return;
     double* __restrict__ o = IL4 ? out + (stream >> 5) * 32 * ld + (stream & 31) * 4 : out + stream * ld;
     double* cv = sh_vals[warp];
@@ -295,15 +299,21 @@ extern "C" int cs_exp_streams_impl(const uint64_t* d_keys, int64_t n_streams, in
 // Streams plus the segmented simulator's arrival-time prefix (jffc_seg.cu).
 extern "C" int cs_exp_streams_prefix_impl(const uint64_t* d_keys, int64_t n_streams, int64_t n_draws,
                                           double* d_out, int64_t ld, int log1p_fma,
-                                          const cs::PrefixPlan* plan, int il4, void* stream) {
+                                          const cs::PrefixPlan* plan, int il4, int whole_sm, void* stream) {
     if (n_streams <= 0 || n_draws <= 0) return 0;
-    const int64_t blocks = (n_streams + cs::EXP_WARPS - 1) / cs::EXP_WARPS;
+    const int w = whole_sm ? 16 : 8;
+    const int64_t blocks = (n_streams + w - 1) / w;
     cudaStream_t st = (cudaStream_t)stream;
-    if (il4)
-        cs::exp_streams_prefix_kernel<true><<<(unsigned)blocks, cs::EXP_WARPS * 32, 0, st>>>(
-            d_keys, n_streams, n_draws, d_out, ld, log1p_fma, *plan);
+#define CS_PFX(IL, W) \
+    cs::exp_streams_prefix_kernel<IL, W><<<(unsigned)blocks, W * 32, 0, st>>>(d_keys, n_streams, n_draws, d_out, ld, log1p_fma, *plan)
+    if (il4 && whole_sm)
+        CS_PFX(true, 16);
+    else if (il4)
+        CS_PFX(true, 8);
+    else if (whole_sm)
+        CS_PFX(false, 16);
     else
-        cs::exp_streams_prefix_kernel<false><<<(unsigned)blocks, cs::EXP_WARPS * 32, 0, st>>>(
-            d_keys, n_streams, n_draws, d_out, ld, log1p_fma, *plan);
+        CS_PFX(false, 8);
+#undef CS_PFX
     return cs::check_launch("exp_streams_prefix_kernel");
 }

@@ -103,13 +103,14 @@ class SweepEngine:
                 "flags": C.c_int32(0)}  # simulation flags cs_sim_streams returns
 
     # -- stages (buffer set b, CUDA stream st) ------------------------------
-    def streams(self, b: int = 0, st=None):
+    def streams(self, b: int = 0, st=None, whole_sm: bool = False):
         st = st or self.stream
         B = self.sets[b]
-        rc = self.lib.cs_sim_streams(self.d_keys.data_ptr(), self.R, self.lds, B["S"].data_ptr(), self.lds,
-                                     self.log1p_variant, self.d_pts.data_ptr(), self.P, self.max_chains,
-                                     self.max_cap, self.n, self.warm, B["ws"].data_ptr(), self.ws_bytes,
-                                     C.byref(B["flags"]), st.cuda_stream)
+        rc = self.lib.cs_sim_streams_ex(self.d_keys.data_ptr(), self.R, self.lds, B["S"].data_ptr(), self.lds,
+                                        self.log1p_variant, self.d_pts.data_ptr(), self.P, self.max_chains,
+                                        self.max_cap, self.n, self.warm, B["ws"].data_ptr(), self.ws_bytes,
+                                        N.CS_STREAMS_WHOLE_SM if whole_sm else 0, C.byref(B["flags"]),
+                                        st.cuda_stream)
         N.check(rc, "cs_sim_streams")
 
     def simulate(self, b: int = 0, st=None):
@@ -132,83 +133,45 @@ class SweepEngine:
                 None, st.cuda_stream)
         N.check(rc, "cs_rep_stats")
 
-    def run_pipelined(self, steps: int, after_stats=None, ordered: bool | None = None) -> int:
-        """`steps` complete sweeps, software-pipelined over two buffer sets and
-        three CUDA streams: the streams of sweep k+1 and the statistics of
-        sweep k-1 run while sweep k simulates (the simulator leaves most issue
-        slots idle: one latency-bound warp per scheduler).  Every sweep is
-        computed in full; the caller's stream waits for all of them.
-        ``after_stats(b, stream)`` runs after each sweep's statistics (e.g. the
-        cross-GPU gather of its summaries).  Returns the last sweep's set."""
+    def run_pipelined(self, steps: int, after_stats=None) -> int:
+        """`steps` complete sweeps over two buffer sets and two CUDA streams,
+        in one deterministic order per sweep k: the simulation (alone on the
+        GPU: its cooperative launch keeps one block per resident slot on every
+        SM), then -- beside each other -- the statistics of sweep k and the
+        exponential streams of sweep k+1.  The stream kernel fills whole SMs
+        (16 warps per block, ceil(R/16) blocks) and its stream has the higher
+        priority, so it takes its SMs the moment the simulation ends and the
+        statistics pass runs on the rest.  Every sweep is computed in full;
+        the caller's stream waits for all of them.  ``after_stats(b, stream)``
+        runs after each sweep's statistics (e.g. the cross-GPU gather of its
+        summaries; the statistics' NCCL collectives are in the same stream).
+        Returns the last sweep's set."""
         torch = self.torch
         if len(self.sets) < 2:
             self.sets.append(self._alloc_set())
-            # the simulator's stream has the higher priority: when sweep k-1
-            # ends, sweep k's blocks (resident for the whole sweep) must be
-            # spread over all SMs before the statistics of sweep k-1 take any
-            # -- blocks placed on the few SMs the statistics left free would
-            # pile up there and stretch the simulation several-fold
-            # (lower number = higher priority; torch clamps to the device's range)
-            self.pipe = [torch.cuda.Stream(priority=0), torch.cuda.Stream(priority=-8),
-                         torch.cuda.Stream(priority=0)]
-        s_gen, s_sim, s_stat = self.pipe
-        if ordered is None:
-            ordered = self.distributed or bool(os.environ.get("CS_PIPE_ORDERED"))
+            # lower number = higher priority (torch clamps to the device's range)
+            self.pipe = [torch.cuda.Stream(priority=-8), torch.cuda.Stream(priority=0)]
+        s_gen, s_sim = self.pipe
         cur = torch.cuda.current_stream()
         for s_ in self.pipe:
             s_.wait_stream(cur)
         ev_sim = [torch.cuda.Event(), torch.cuda.Event()]
-        ev_stat = [torch.cuda.Event(), torch.cuda.Event()]
         ev_gen = [torch.cuda.Event(), torch.cuda.Event()]
-        def gen(k):  # streams of sweep k into set k & 1 (free once sweep k-2 simulated)
-            b = k & 1
-            if k >= 2:
-                s_gen.wait_event(ev_sim[b])
-            self.streams(b, s_gen)
-            ev_gen[b].record(s_gen)
-
         if steps > 0:
-            gen(0)
-        if ordered:
-            # sharded: the statistics' NCCL collectives cannot run beside the
-            # simulator (their kernels need an SM configuration the simulator's
-            # SMs do not offer), so they follow each simulation in its stream;
-            # the next sweep's streams run beside these statistics, not beside
-            # the simulation (overlapping the simulation measured 56-71 ms per
-            # sweep at N=4 against 45 ms: the streams' blocks, placed first,
-            # unbalance the simulator's)
-            for k in range(steps):
-                b = k & 1
-                s_sim.wait_event(ev_gen[b])
-                self.simulate(b, s_sim)
-                ev_sim[b].record(s_sim)
-                if k + 1 < steps:
-                    s_gen.wait_event(ev_sim[b])
-                    self.streams((k + 1) & 1, s_gen)
-                    ev_gen[(k + 1) & 1].record(s_gen)
-                self.statistics(b, s_sim)
-                if after_stats is not None:
-                    after_stats(b, s_sim)
-            for s_ in self.pipe:
-                cur.wait_stream(s_)
-            return (steps - 1) & 1
-        for k in range(steps + 1):
-            if k < steps:
-                b = k & 1
-                s_sim.wait_event(ev_gen[b])
-                if k >= 2:
-                    s_sim.wait_event(ev_stat[b])  # response buffer b read by sweep k-2
-                self.simulate(b, s_sim)
-                ev_sim[b].record(s_sim)
-                if k + 1 < steps:  # enqueued before the (host-blocking) statistics below
-                    gen(k + 1)
-            if k >= 1:
-                bb = (k - 1) & 1
-                s_stat.wait_event(ev_sim[bb])
-                self.statistics(bb, s_stat)
-                if after_stats is not None:
-                    after_stats(bb, s_stat)
-                ev_stat[bb].record(s_stat)
+            self.streams(0, s_gen)
+            ev_gen[0].record(s_gen)
+        for k in range(steps):
+            b = k & 1
+            s_sim.wait_event(ev_gen[b])
+            self.simulate(b, s_sim)
+            ev_sim[b].record(s_sim)
+            if k + 1 < steps:  # set (k+1)&1 was last read by sweep k-1 (done before sweep k)
+                s_gen.wait_event(ev_sim[b])
+                self.streams((k + 1) & 1, s_gen, whole_sm=True)
+                ev_gen[(k + 1) & 1].record(s_gen)
+            self.statistics(b, s_sim)
+            if after_stats is not None:
+                after_stats(b, s_sim)
         for s_ in self.pipe:
             cur.wait_stream(s_)
         return (steps - 1) & 1

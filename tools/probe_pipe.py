@@ -13,21 +13,20 @@ def main():
     import paper_2604_14993_b200 as P
     from paper_2604_14993_b200.engine import SweepEngine
 
-    ordered = os.environ.get("ORDERED", "1") == "1"
     service, servers, _ = P.petals_instance(10, 0.2, 101)
     s = P.greedy_cache_allocation(P.greedy_block_placement(servers, service, 7, 0.2, 0.7).placement)
     lams = [s.total_rate * x for x in np.linspace(0.05, 0.95, 16)]
     e = SweepEngine([s.rates] * 16, [s.capacities] * 16, lams, 100000, 0.1, 1, 1024)
-    e.run_pipelined(3, ordered=ordered)
+    e.run_pipelined(3)
     torch.cuda.synchronize()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
-    e.run_pipelined(6, ordered=ordered)
+    e.run_pipelined(6)
     b.record()
     b.synchronize()
     print("pipelined ms/step", a.elapsed_time(b) / 6)
     with profile(activities=[ProfilerActivity.CUDA]) as prof:
-        e.run_pipelined(4, ordered=ordered)
+        e.run_pipelined(4)
         torch.cuda.synchronize()
     evs = [x for x in prof.events() if x.device_type.name == "CUDA"]
     t0 = min(x.time_range.start for x in evs)
