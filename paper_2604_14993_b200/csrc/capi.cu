@@ -229,7 +229,8 @@ int cs_jffc_sim_ex(const cs_sim_point* d_points, int32_t n_points, const double*
         set_error("cs_jffc_sim: invalid sizes");
         return CS_INVALID;
     }
-    if ((flags & CS_SIM_STREAMS_IL4) && (d_jobs != nullptr || !cs::use_seg(max_chains, max_capacity, n_jobs))) {
+    if ((flags & CS_SIM_STREAMS_IL4) && (d_jobs != nullptr || (flags & CS_SIM_FORCE_EVENT_LOOP) ||
+                                         !cs::use_seg(max_chains, max_capacity, n_jobs))) {
         set_error("cs_jffc_sim: interleaved streams are read by the segmented path only");
         return CS_INVALID;
     }
