@@ -104,7 +104,16 @@ def run_sim_sharded(configs: Sequence[SimConfig]) -> list[SimStats]:
                       c0.seed, count, rep_begin=begin, distributed=world > 1,
                       total_reps=c0.replications)
     eng.step()
-    summ = _gather_device_rows(eng.sets[0]["summ"], N.SUMMARY_DTYPE, (eng.P, eng.R))   # [P, R]
-    busy = _gather_device_rows(eng.sets[0]["busy"], np.float64, (eng.P, eng.R, eng.ldb))
-    order = eng.order_stats()
-    return _stats_from_batch(configs, summ, busy, order, None)
+    return merge_sharded(configs, eng.sets[0]["summ"], eng.sets[0]["busy"], eng.order_stats(), eng.ldb)
+
+
+def merge_sharded(configs: Sequence[SimConfig], local_summ, local_busy, order_stats, ldb: int) -> list[SimStats]:
+    """The sharded sweep's host side: every rank's [P, R/world] summaries and
+    busy times (tensors in the engine's layout) gathered in rank order along
+    the replication axis, then the reference's aggregation over all
+    replications (order_stats are already global: cs_rep_stats_dist)."""
+    rank, world = rank_world()
+    P, R = len(configs), configs[0].replications // world
+    summ = _gather_device_rows(local_summ, N.SUMMARY_DTYPE, (P, R))   # [P, R_total]
+    busy = _gather_device_rows(local_busy, np.float64, (P, R, ldb))
+    return _stats_from_batch(configs, summ, busy, order_stats, None)
