@@ -511,7 +511,7 @@ __global__ void __launch_bounds__(1024) round_select_kernel(SelSlot* __restrict_
 // ---------------------------------------------------------------------------
 // CS_TRACE_STATS=1: host timestamps at the statistics' phase boundaries
 static void trace(const char* what, cudaStream_t st) {
-    static const bool on = getenv("CS_TRACE_STATS") != nullptr;
+    const bool on = getenv("CS_TRACE_STATS") != nullptr;
     if (!on) return;
     static double t0 = 0;
     cudaStreamSynchronize(st);

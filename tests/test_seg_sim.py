@@ -179,3 +179,21 @@ def test_stream_layouts_vs_oracle(eng, oracle, R):
     got = e.summaries(0)
     for f in ("wait_sum", "mean_occupancy", "end_queue_len", "resp_mean"):
         assert np.array_equal(np.asarray(got[f]).view(np.uint64), np.asarray(res.summaries[f]).view(np.uint64)), f
+
+
+def test_instrumentation_switches_keep_results(eng, monkeypatch, capfd):
+    """The development switches (CS_SEG_TRACE: the simulator's per-segment
+    timeline; CS_TRACE_STATS: the statistics' phase times; CS_DEBUG_STATS)
+    only print to stderr: every output is unchanged."""
+    system = _petals(eng)
+    lams = [system.total_rate * x for x in (0.3, 0.9)]
+    args = ([system.rates] * 2, [system.capacities] * 2, lams, 30_000, 0.1, 9, 64)
+    ref = eng.simulate_sweep(*args)
+    for var in ("CS_SEG_TRACE", "CS_TRACE_STATS", "CS_DEBUG_STATS"):
+        monkeypatch.setenv(var, "1")
+    got = eng.simulate_sweep(*args)
+    err = capfd.readouterr().err
+    assert "jffc_seg_kernel" in err and "[stats]" in err
+    assert np.array_equal(got.summaries.view(np.uint8), ref.summaries.view(np.uint8))
+    assert np.array_equal(bits(got.busy), bits(ref.busy))
+    assert got.order_stats == ref.order_stats
