@@ -212,9 +212,9 @@ __global__ void __launch_bounds__(256) compact_bucket_kernel(
                     for (int q = 0; q < SEL_LISTS; q++)
                         if (bk[q] == d0) ql = q;
                 }
-                if (__any_sync(0xffffffffu, ql >= 0))
-                    for (int q = 0; q < nl; q++)
-                        cand_push(cc, lane, q, ql, v[k], fill + gl0, cap + gl0, off + gl0, cand);
+                // only the lists some lane appends to (usually one)
+                for (unsigned m = __reduce_or_sync(0xffffffffu, ql >= 0 ? 1u << ql : 0u); m; m &= m - 1)
+                    cand_push(cc, lane, __ffs(m) - 1, ql, v[k], fill + gl0, cap + gl0, off + gl0, cand);
             }
         }
     }
