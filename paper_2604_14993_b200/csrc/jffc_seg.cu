@@ -620,20 +620,54 @@ __global__ void __launch_bounds__(32, CS_SEG_MINB) jffc_seg_kernel(Args A) {
     if (tr && lane == 0) tr[2] = gtimer();
     int t = s + 1;
     while (__any_sync(FULL, act)) {
-        // entering segment t's range: its phase-1 writes (responses, blocks)
-        // must be complete before ours overwrite them
+        // Entering segment t's range while t may still run its phase 1: every
+        // write into its range must land after t's own write of the same
+        // place.  t publishes at checkpoint q (release) its blocks up to job
+        // bt + ck_offset(q) and, per row, its emission count there -- the
+        // complete lines below it are flushed; DONE publishes everything.
+        // So: run a chunk only up to t's latest published job (blocks and
+        // checkpoints there exist), flush only lines below t's flushed
+        // frontier, and hand over at a coupling only once t has flushed past
+        // our emissions (t's still-unflushed pre-coupling values would
+        // otherwise land after ours).  t never waits for us: no deadlock.
         const uint32_t* prog = A.progress + (int64_t)t * G + g;
-        while (!(ld_relaxed(prog) & DONE)) __nanosleep(256);
-        fence_acquire();
         const int64_t bt = seg_begin(t, S, n), et = seg_begin(t + 1, S, n);
         const double* tcf = A.ckf + (((int64_t)t * G + g) * Q) * FCK * 32 + lane;
         const uint32_t* tck = A.ckk + (((int64_t)t * G + g) * Q) * CMAX * 32 + lane;
+        uint32_t qt = 0;                 // t's latest checkpoint seen
+        int64_t jt = bt;                 // t's blocks / checkpoints exist up to here
+        int32_t ft = INT32_MIN;          // t's flushed frontier for this lane's row
+        auto refresh = [&]() {
+            const uint32_t pv = ld_relaxed(prog);
+            if (pv & DONE) {
+                if (jt != INT64_MAX) {
+                    fence_acquire();
+                    jt = INT64_MAX;
+                    ft = INT32_MAX;
+                }
+            } else if (pv > qt) {
+                fence_acquire();
+                qt = pv;
+                jt = bt + ck_offset((int)qt);
+                ft = (int32_t)__double_as_longlong(__ldcg(tcf + (int64_t)(qt - 1) * FCK * 32 + CMAX * 32)) & ~15;
+            }
+        };
+        auto wait_for = [&](auto ok) {  // warp-uniform: until every lane's condition holds
+            if (__all_sync(FULL, ok())) return;
+            refresh();
+            while (!__all_sync(FULL, ok())) {
+                __nanosleep(256);
+                refresh();
+            }
+        };
         int q = 1;
         int64_t next_ck = Q >= 1 ? bt + ck_offset(1) : INT64_MAX;
         while (j < et && __any_sync(FULL, act)) {
             const int64_t jn = (j + 16 < et) ? j + 16 : et;
+            wait_for([&] { return jn <= jt; });
             prefetch();
             run_to(jn);
+            wait_for([&] { return !act || (n_resp & ~15) <= ft; });
             flush(false, act);
             if (j % (int32_t)BS == 0 || j == n) put_block(act);
             if (j == next_ck) {
@@ -648,6 +682,7 @@ __global__ void __launch_bounds__(32, CS_SEG_MINB) jffc_seg_kernel(Args A) {
                     same = same && __double_as_longlong(__ldcg(cf + CMAX * 32)) == (int64_t)n_resp;
                 }
                 if (__any_sync(FULL, same)) {
+                    wait_for([&] { return !same || n_resp <= ft; });
                     flush(true, same);  // our emissions before the hand-over
                     if (same) {
                         st_release(A.status + (int64_t)t * T + tid, (int32_t)(2 + j));
@@ -659,6 +694,7 @@ __global__ void __launch_bounds__(32, CS_SEG_MINB) jffc_seg_kernel(Args A) {
             }
         }
         if (j == et && __any_sync(FULL, act)) {
+            wait_for([&] { return jt == INT64_MAX; });  // t's range entirely ours from here
             if (et == n) {  // ran through the last segment: these lanes finish the row
                 drain(act);
                 flush(true, act);
