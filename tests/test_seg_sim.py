@@ -197,3 +197,22 @@ def test_instrumentation_switches_keep_results(eng, monkeypatch, capfd):
     assert np.array_equal(got.summaries.view(np.uint8), ref.summaries.view(np.uint8))
     assert np.array_equal(bits(got.busy), bits(ref.busy))
     assert got.order_stats == ref.order_stats
+
+
+def test_random_shapes_vs_oracle(eng, oracle):
+    """Seeded random shapes (points, replications, jobs, capacity, rate, load,
+    warm-up) through the segmented path, every field against the oracle --
+    the hand-over between segments under every mix of coupling lengths."""
+    rng = np.random.default_rng(20260419)
+    for _ in range(40):
+        P = int(rng.integers(1, 20))
+        R = int(rng.choice([1, 3, 31, 32, 33, 64]))
+        n = int(rng.integers(3_000, 60_000))
+        C = int(rng.integers(1, 17))
+        rate = float(rng.uniform(0.3, 2.0))
+        wf = float(rng.choice([0.0, 0.1, 0.37]))
+        seed = int(rng.integers(0, 2**31))
+        lams = [float(rng.uniform(0.05, 1.15)) * rate * C for _ in range(P)]
+        res = eng.simulate_sweep([(rate,)] * P, [(C,)] * P, lams, n, wf, seed, R, return_responses=True)
+        for p in {0, P - 1, P // 2}:
+            _check_rows(res, p, oracle, (rate,), (C,), lams[p], n, wf, seed, R)
