@@ -19,6 +19,8 @@ extern "C" int cs_jffc_sim_impl(const cs_sim_point*, int32_t, const double*, con
                                 void*, int64_t, int32_t, void*);
 extern "C" int cs_exp_streams_prefix_impl(const uint64_t*, int64_t, int64_t, double*, int64_t, int,
                                           const cs::PrefixPlan*, int, int, void*);
+extern "C" int cs_exp_streams_il4_p1_impl(const uint64_t*, int64_t, int64_t, double*, int64_t, int,
+                                          const cs::PrefixPlan*, void*);
 extern "C" bool cs_seg_prefix_plan(int32_t, int32_t, int32_t, int64_t, int64_t, const cs_sim_point*, void*,
                                    cs::PrefixPlan*);
 namespace cs {
@@ -280,8 +282,12 @@ int cs_sim_streams_ex(const uint64_t* d_keys, int64_t n_streams, int64_t n_draws
         cs_seg_prefix_plan(n_points, (int32_t)n_streams, max_capacity, n_jobs, warm, d_points, d_workspace, &pp)) {
         // few points per stream: every simulator lane reads its own row
         const bool il4 = n_points < 16 && n_streams % 32 == 0 && ld % 4 == 0;
-        const int rc = cs_exp_streams_prefix_impl(d_keys, n_streams, n_draws, d_out, ld, v, &pp, il4,
-                                                  (opts & CS_STREAMS_WHOLE_SM) ? 1 : 0, stream);
+        // one point per stream: the prefix chain in its own pass (one thread
+        // per stream) instead of one lane of each generating warp
+        const int rc = (il4 && n_points == 1)
+                           ? cs_exp_streams_il4_p1_impl(d_keys, n_streams, n_draws, d_out, ld, v, &pp, stream)
+                           : cs_exp_streams_prefix_impl(d_keys, n_streams, n_draws, d_out, ld, v, &pp, il4,
+                                                        (opts & CS_STREAMS_WHOLE_SM) ? 1 : 0, stream);
         if (rc == CS_OK) *sim_flags = CS_SIM_PREFIX_READY | (il4 ? CS_SIM_STREAMS_IL4 : 0);
         return rc;
     }

@@ -156,24 +156,113 @@ __device__ __forceinline__ int64_t gen_stream(const ZigSmem* zs, int lane, uint6
 // block shape barely matters (4 per block measured 2% slower than 8)
 constexpr int EXP_WARPS = 8;
 
+// The simulator's interleaved stream layout (jffc_seg.cu il4_off): stream r's
+// value i at (r / 32) * 32 * ld + (i / 4) * 128 + (r % 32) * 4 + i % 4.
+__device__ __forceinline__ int64_t il4_pos(int64_t i) { return ((i >> 2) << 7) + (i & 3); }
+
+// IL4: the interleaved layout, each chunk written in order from a per-warp
+// buffer (4 consecutive lanes fill one 32-byte sector).
+template <bool IL4>
 __global__ void __launch_bounds__(EXP_WARPS * 32) exp_streams_kernel(const uint64_t* __restrict__ keys,
                                                                      int64_t n_streams, int64_t n_draws,
                                                                      double* __restrict__ out, int64_t ld,
                                                                      int log1p_fma) {
     __shared__ ZigSmem zs;
+    __shared__ double sh_vals[IL4 ? EXP_WARPS : 1][136];
     zig_load(&zs);
     __syncthreads();
     const int lane = threadIdx.x & 31;
     const int64_t stream = (int64_t)blockIdx.x * EXP_WARPS + (threadIdx.x >> 5);
     if (stream >= n_streams) return;
-    double* __restrict__ o = out + stream * ld;
+    double* __restrict__ o = IL4 ? out + (stream >> 5) * 32 * ld + (stream & 31) * 4 : out + stream * ld;
+    double* cv = sh_vals[IL4 ? (threadIdx.x >> 5) : 0];
     int64_t base = 0;
     gen_stream(
         &zs, lane, keys[2 * stream], keys[2 * stream + 1], n_draws, log1p_fma,
         [&](int i, double x) {
-            if (base + i < n_draws) o[base + i] = x;
+            if (IL4)
+                cv[i] = x;
+            else if (base + i < n_draws)
+                o[base + i] = x;
         },
-        [&](int64_t produced, int tot) { base = produced + tot; });
+        [&](int64_t produced, int tot) {
+            if (IL4) {
+                __syncwarp();
+                for (int i = lane; i < tot; i += 32) {
+                    const int64_t q = produced + i;
+                    if (q < n_draws) o[il4_pos(q)] = cv[i];
+                }
+                __syncwarp();
+            }
+            base = produced + tot;
+        });
+}
+
+// The arrival-time prefix of single-point streams (P = 1, interleaved): one
+// thread per stream runs the exact np.cumsum chain a_j = a_{j-1} + (1/lam) *
+// S_j over its gaps and records a_j at the listed job indices.  Fused into
+// the generating warp this chain (8 cycles per job on one lane, the loop
+// issued by the whole warp) nearly doubled the config-5 stream kernel; alone
+// it runs near the DADD latency: the gaps are staged through a per-thread
+// cp.async ring in shared memory laid out [batch slot][gap pair][thread]
+// (16-byte pieces: a warp's shared reads are conflict-free).
+constexpr int PR_B = 32, PR_NBUF = 16, PR_THREADS = 32;
+__global__ void __launch_bounds__(PR_THREADS) prefix_p1_kernel(const double* __restrict__ S, int64_t n_streams,
+                                                               int64_t ld, const PrefixPlan pp) {
+    extern __shared__ __align__(16) double2 pr_ring[];  // [PR_NBUF][PR_B / 2][PR_THREADS]
+    const int lane = threadIdx.x;
+    const int64_t r = (int64_t)blockIdx.x * PR_THREADS + lane;
+    const bool valid = r < n_streams;
+    const double* __restrict__ src = S + (valid ? (r >> 5) * 32 * ld + (r & 31) * 4 : 0);
+    const double sc = __ddiv_rn(1.0, pp.pts[0].lam);
+    const int64_t n = pp.n_cum;
+    const int64_t nb = (n + PR_B - 1) / PR_B;
+    const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(pr_ring);
+    auto issue = [&](int64_t b) {
+        if (valid && b < nb) {
+            const uint32_t d = ring_s + (uint32_t)(((b % PR_NBUF) * (PR_B / 2) * PR_THREADS + lane) * 16);
+#pragma unroll
+            for (int k = 0; k < PR_B / 2; k++)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d + k * PR_THREADS * 16),
+                             "l"(src + il4_pos(b * PR_B + 2 * k))
+                             : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    for (int b = 0; b < PR_NBUF - 1; b++) issue(b);
+    double a = 0.0;
+    int ev = 0;
+    for (int64_t b = 0; b < nb; b++) {
+        issue(b + PR_NBUF - 1);
+        asm volatile("cp.async.wait_group %0;" ::"n"(PR_NBUF - 1) : "memory");
+        const double2* x = pr_ring + (b % PR_NBUF) * (PR_B / 2) * PR_THREADS + lane;
+        double v[PR_B];
+#pragma unroll
+        for (int k = 0; k < PR_B / 2; k++) {
+            const double2 t = x[k * PR_THREADS];
+            v[2 * k] = __dmul_rn(sc, t.x);
+            v[2 * k + 1] = __dmul_rn(sc, t.y);
+        }
+        const int64_t j0 = b * PR_B;
+        const bool evb = ev < pp.nev && pp.ev_idx[ev] < j0 + PR_B;
+        if (!evb && j0 > 0 && j0 + PR_B <= n) {
+#pragma unroll
+            for (int k = 0; k < PR_B; k++) a = __dadd_rn(a, v[k]);
+        } else {
+#pragma unroll
+            for (int k = 0; k < PR_B; k++) {
+                const int64_t j = j0 + k;
+                if (j < n) {
+                    a = j == 0 ? v[k] : __dadd_rn(a, v[k]);
+                    while (ev < pp.nev && pp.ev_idx[ev] == j) {
+                        if (valid) pp.out[r * pp.ncol + pp.ev_col[ev]] = a;
+                        ev++;
+                    }
+                }
+            }
+        }
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
 // Streams plus the segmented simulator's arrival-time prefix (jffc_seg.cu):
@@ -187,10 +276,8 @@ __global__ void __launch_bounds__(EXP_WARPS * 32) exp_streams_kernel(const uint6
 // prefix lanes of one warp serve several streams in lockstep and stall the
 // producers, 3.9 -> 5.9 ms on config 2, 56 -> 192 ms per 2048 config-5 streams.)
 //
-// IL4: the output in the simulator's interleaved layout (jffc_seg.cu il4_off):
-// stream r's value i at (r / 32) * 32 * ld + (i / 4) * 128 + (r % 32) * 4 + i % 4,
-// written from the chunk buffer in order.
-__device__ __forceinline__ int64_t il4_pos(int64_t i) { return ((i >> 2) << 7) + (i & 3); }
+// IL4: the output in the interleaved layout, written from the chunk buffer in
+// order.
 
 // W streams per block.  W = 16 (whole_sm): a block fills one SM's register
 // file, so the kernel occupies ceil(R / 16) whole SMs and leaves the others to
@@ -291,9 +378,27 @@ extern "C" int cs_exp_streams_impl(const uint64_t* d_keys, int64_t n_streams, in
                                    double* d_out, int64_t ld, int log1p_fma, void* stream) {
     if (n_streams <= 0 || n_draws <= 0) return 0;
     const int64_t blocks = (n_streams + cs::EXP_WARPS - 1) / cs::EXP_WARPS;
-    cs::exp_streams_kernel<<<(unsigned)blocks, cs::EXP_WARPS * 32, 0, (cudaStream_t)stream>>>(
+    cs::exp_streams_kernel<false><<<(unsigned)blocks, cs::EXP_WARPS * 32, 0, (cudaStream_t)stream>>>(
         d_keys, n_streams, n_draws, d_out, ld, log1p_fma);
     return cs::check_launch("exp_streams_kernel");
+}
+
+// Single-point interleaved streams: generation, then the prefix pass.
+extern "C" int cs_exp_streams_il4_p1_impl(const uint64_t* d_keys, int64_t n_streams, int64_t n_draws,
+                                          double* d_out, int64_t ld, int log1p_fma, const cs::PrefixPlan* plan,
+                                          void* stream) {
+    if (n_streams <= 0 || n_draws <= 0) return 0;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t blocks = (n_streams + cs::EXP_WARPS - 1) / cs::EXP_WARPS;
+    cs::exp_streams_kernel<true><<<(unsigned)blocks, cs::EXP_WARPS * 32, 0, st>>>(d_keys, n_streams, n_draws,
+                                                                                  d_out, ld, log1p_fma);
+    int rc = cs::check_launch("exp_streams_kernel<il4>");
+    if (rc) return rc;
+    const size_t smem = sizeof(double) * cs::PR_NBUF * cs::PR_B * cs::PR_THREADS;
+    cudaFuncSetAttribute(cs::prefix_p1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cs::prefix_p1_kernel<<<(unsigned)((n_streams + cs::PR_THREADS - 1) / cs::PR_THREADS), cs::PR_THREADS, smem,
+                           st>>>(d_out, n_streams, ld, *plan);
+    return cs::check_launch("prefix_p1_kernel");
 }
 
 // Streams plus the segmented simulator's arrival-time prefix (jffc_seg.cu).
