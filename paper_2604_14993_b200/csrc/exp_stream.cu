@@ -153,7 +153,10 @@ __device__ __forceinline__ int64_t gen_stream(const ZigSmem* zs, int lane, uint6
 }
 
 // streams (warps) per block; each warp's chunk loop is latency-bound, so the
-// block shape barely matters (4 per block measured 2% slower than 8)
+// block shape barely matters (4 per block measured 2% slower than 8), but two
+// blocks must fit one SM: capped at 128 registers (unbounded, the IL4 variant
+// took 134 -> one block per SM, config 5's 4096 streams in 4 waves instead of
+// 2: 119 -> 83 ms per chunk)
 constexpr int EXP_WARPS = 8;
 
 // The simulator's interleaved stream layout (jffc_seg.cu il4_off): stream r's
@@ -163,7 +166,7 @@ __device__ __forceinline__ int64_t il4_pos(int64_t i) { return ((i >> 2) << 7) +
 // IL4: the interleaved layout, each chunk written in order from a per-warp
 // buffer (4 consecutive lanes fill one 32-byte sector).
 template <bool IL4>
-__global__ void __launch_bounds__(EXP_WARPS * 32) exp_streams_kernel(const uint64_t* __restrict__ keys,
+__global__ void __launch_bounds__(EXP_WARPS * 32, 2) exp_streams_kernel(const uint64_t* __restrict__ keys,
                                                                      int64_t n_streams, int64_t n_draws,
                                                                      double* __restrict__ out, int64_t ld,
                                                                      int log1p_fma) {
