@@ -52,6 +52,34 @@ __device__ __forceinline__ void philox4x64_10(uint64_t c0, uint64_t c1, uint64_t
     out[3] = c3;
 }
 
+// The 10 round keys of one stream, staged in shared memory by its warp
+// (ks[r] = {k0 + r*W0, k1 + r*W1}): held in registers they took 40 of the
+// stream kernels' 128, and the slow-attempt loop then spilled.
+__device__ __forceinline__ void philox_key_schedule(ulonglong2* ks, int lane, uint64_t k0, uint64_t k1) {
+    if (lane < 10) ks[lane] = make_ulonglong2(k0 + (uint64_t)lane * PH_W0, k1 + (uint64_t)lane * PH_W1);
+    __syncwarp();
+}
+
+// Philox4x64-10 of counter {c0,0,0,0} with the round keys read from ks.
+__device__ __forceinline__ void philox4x64_10_ks(uint64_t c0, const ulonglong2* ks, uint64_t out[4]) {
+    uint64_t c1 = 0, c2 = 0, c3 = 0;
+#pragma unroll
+    for (int r = 0; r < 10; r++) {
+        const ulonglong2 k = ks[r];
+        const uint64_t lo0 = PH_M0 * c0, hi0 = __umul64hi(PH_M0, c0);
+        const uint64_t lo1 = PH_M1 * c2, hi1 = __umul64hi(PH_M1, c2);
+        const uint64_t n0 = hi1 ^ c1 ^ k.x, n2 = hi0 ^ c3 ^ k.y;
+        c0 = n0;
+        c1 = lo1;
+        c2 = n2;
+        c3 = lo0;
+    }
+    out[0] = c0;
+    out[1] = c1;
+    out[2] = c2;
+    out[3] = c3;
+}
+
 // Ziggurat tables staged in shared memory (random per-lane layer index).
 struct ZigSmem {
     double we[256];
@@ -87,7 +115,7 @@ __device__ __forceinline__ bool zig_fast(const ZigSmem* z, uint64_t w, double* x
     return ri < z->ke[idx];
 }
 
-__device__ __noinline__ ZigAttempt zig_slow(const ZigSmem* z, uint64_t w, uint64_t w2,
+__device__ __forceinline__ ZigAttempt zig_slow(const ZigSmem* z, uint64_t w, uint64_t w2,
                                             int log1p_fma) {
     const uint64_t ri = w >> 11;
     const int idx = (int)((w >> 3) & 0xFF);

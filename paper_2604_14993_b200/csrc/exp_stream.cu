@@ -33,7 +33,7 @@ struct Xfer {
 // the stream's values before this chunk, tot = this chunk's count; emitted
 // values may run past n_draws, the callbacks clip).
 template <typename Emit, typename Done>
-__device__ __forceinline__ int64_t gen_stream(const ZigSmem* zs, int lane, uint64_t k0, uint64_t k1,
+__device__ __forceinline__ int64_t gen_stream(const ZigSmem* zs, int lane, const ulonglong2* ks,
                                               int64_t n_draws, int log1p_fma, Emit&& emit, Done&& chunk_done) {
     int64_t produced = 0;
     int entry = 0;        // warp-uniform: offset of the first attempt in this chunk
@@ -43,43 +43,51 @@ __device__ __forceinline__ int64_t gen_stream(const ZigSmem* zs, int lane, uint6
     // multiply chain per lane) are computed while this chunk is classified,
     // scanned and emitted
     uint64_t wn[4];
-    philox4x64_10(lane + 1, 0, 0, 0, k0, k1, wn);
+    philox4x64_10_ks(lane + 1, ks, wn);
     while (produced < n_draws) {
         uint64_t w[4];
 #pragma unroll
         for (int q = 0; q < 4; q++) w[q] = wn[q];
-        philox4x64_10((chunk + 1) * 32 + lane + 1, 0, 0, 0, k0, k1, wn);
+        philox4x64_10_ks((chunk + 1) * 32 + lane + 1, ks, wn);
         const uint64_t wnext = __shfl_down_sync(0xffffffffu, w[0], 1);
 
         // Per-word attempt results.
         double v[4];
         int adv[4];
         bool has[4];
+        // Fast accepts first; a lane's slow attempts (about one word in 90:
+        // 3/4 of the chunks have one somewhere in the warp) then run in ONE
+        // loop, so a chunk pays the divergent slow path about once instead
+        // of once per word position.  Bit 4: the attempt carried from the
+        // previous chunk (lane 0, entry 1), resolved with this chunk's word 0.
+        unsigned slow = lane == 0 && entry == 1 ? 16u : 0u;
 #pragma unroll
         for (int p = 0; p < 4; p++) {
             double x;
-            if (zig_fast(zs, w[p], &x)) {
-                v[p] = x;
-                adv[p] = 1;
-                has[p] = true;
-            } else if (p < 3 || lane < 31) {
-                const ZigAttempt a = zig_slow(zs, w[p], p < 3 ? w[p + 1] : wnext, log1p_fma);
-                v[p] = a.v;
-                adv[p] = 2;
-                has[p] = a.has;
-            } else {
-                v[p] = 0.0;  // carried: resolved by the next chunk's lane 0
-                adv[p] = 2;
-                has[p] = false;
-            }
+            const bool f = zig_fast(zs, w[p], &x);
+            v[p] = f ? x : 0.0;  // a slow attempt at word 127 is carried
+            adv[p] = f ? 1 : 2;
+            has[p] = f;
+            if (!f && (p < 3 || lane < 31)) slow |= 1u << p;
         }
-        // Carried slow attempt from the previous chunk (only lane 0, entry 1).
         bool carry_has = false;
         double carry_v = 0.0;
-        if (lane == 0 && entry == 1) {
-            const ZigAttempt a = zig_slow(zs, pend_w, w[0], log1p_fma);
-            carry_has = a.has;
-            carry_v = a.v;
+        while (slow) {
+            const int p = __ffs(slow) - 1;
+            slow &= slow - 1;
+            const uint64_t a = p == 0 ? w[0] : p == 1 ? w[1] : p == 2 ? w[2] : p == 3 ? w[3] : pend_w;
+            const uint64_t b = p == 0 ? w[1] : p == 1 ? w[2] : p == 2 ? w[3] : p == 3 ? wnext : w[0];
+            const ZigAttempt r = zig_slow(zs, a, b, log1p_fma);
+#pragma unroll
+            for (int q = 0; q < 4; q++)
+                if (p == q) {
+                    v[q] = r.v;
+                    has[q] = r.has;
+                }
+            if (p == 4) {
+                carry_v = r.v;
+                carry_has = r.has;
+            }
         }
 
         // Transfer function of this lane.
@@ -172,6 +180,7 @@ __global__ void __launch_bounds__(EXP_WARPS * 32, 2) exp_streams_kernel(const ui
                                                                      int log1p_fma) {
     __shared__ ZigSmem zs;
     __shared__ double sh_vals[IL4 ? EXP_WARPS : 1][136];
+    __shared__ ulonglong2 sh_ks[EXP_WARPS][10];
     zig_load(&zs);
     __syncthreads();
     const int lane = threadIdx.x & 31;
@@ -180,8 +189,10 @@ __global__ void __launch_bounds__(EXP_WARPS * 32, 2) exp_streams_kernel(const ui
     double* __restrict__ o = IL4 ? out + (stream >> 5) * 32 * ld + (stream & 31) * 4 : out + stream * ld;
     double* cv = sh_vals[IL4 ? (threadIdx.x >> 5) : 0];
     int64_t base = 0;
+    ulonglong2* ks = sh_ks[threadIdx.x >> 5];
+    philox_key_schedule(ks, lane, keys[2 * stream], keys[2 * stream + 1]);
     gen_stream(
-        &zs, lane, keys[2 * stream], keys[2 * stream + 1], n_draws, log1p_fma,
+        &zs, lane, ks, n_draws, log1p_fma,
         [&](int i, double x) {
             if (IL4)
                 cv[i] = x;
@@ -292,6 +303,7 @@ __global__ void __launch_bounds__(W * 32, W == 16 ? 1 : 2) exp_streams_prefix_ke
     int64_t ld, int log1p_fma, const PrefixPlan pp) {
     __shared__ ZigSmem zs;
     __shared__ double sh_vals[W][136];  // a chunk's values (<= 128 + carry), per warp
+    __shared__ ulonglong2 sh_ks[W][10];
     zig_load(&zs);
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -306,8 +318,10 @@ __global__ void __launch_bounds__(W * 32, W == 16 ? 1 : 2) exp_streams_prefix_ke
     double a = 0.0;
     int ev = 0;  // next event of the (uniform) event list
     int64_t base = 0;
+    ulonglong2* ks = sh_ks[threadIdx.x >> 5];
+    philox_key_schedule(ks, lane, keys[2 * stream], keys[2 * stream + 1]);
     gen_stream(
-        &zs, lane, keys[2 * stream], keys[2 * stream + 1], n_draws, log1p_fma,
+        &zs, lane, ks, n_draws, log1p_fma,
         [&](int i, double x) {
             cv[i] = x;
             if (!IL4 && base + i < n_draws) o[base + i] = x;
