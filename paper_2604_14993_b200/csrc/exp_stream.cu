@@ -22,17 +22,12 @@
 
 namespace cs {
 
-struct Xfer {
-    int x0, x1;  // exit offset for entry 0 / 1
-    int c0, c1;  // values emitted for entry 0 / 1
-};
-
 // The generator loop of one stream (one warp).  For every chunk, emit(i, v)
 // is called by the lanes holding values (i = index within the chunk, in
 // stream order) and then chunk_done(produced, tot) by every lane (produced =
 // the stream's values before this chunk, tot = this chunk's count; emitted
 // values may run past n_draws, the callbacks clip).
-template <typename Emit, typename Done>
+template <bool SCAN2, typename Emit, typename Done>
 __device__ __forceinline__ int64_t gen_stream(const ZigSmem* zs, int lane, const ulonglong2* ks,
                                               int64_t n_draws, int log1p_fma, Emit&& emit, Done&& chunk_done) {
     int64_t produced = 0;
@@ -90,8 +85,9 @@ __device__ __forceinline__ int64_t gen_stream(const ZigSmem* zs, int lane, const
             }
         }
 
-        // Transfer function of this lane.
-        Xfer f;
+        // Transfer function of this lane: per entry offset e, E_e = exit
+        // offset | values emitted << 1.
+        int e0, e1;
         {
             int p = 0, c = 0;
 #pragma unroll
@@ -100,42 +96,60 @@ __device__ __forceinline__ int64_t gen_stream(const ZigSmem* zs, int lane, const
                     c += has[q];
                     p += adv[q];
                 }
-            f.x0 = p - 4;
-            f.c0 = c;
+            e0 = (p - 4) | (c << 1);
             p = 1;
-            c = 0;
+            c = carry_has ? 1 : 0;
 #pragma unroll
             for (int q = 1; q < 4; q++)
                 if (p == q) {
                     c += has[q];
                     p += adv[q];
                 }
-            f.x1 = p - 4;
-            f.c1 = c + (carry_has ? 1 : 0);
+            e1 = (p - 4) | (c << 1);
         }
-        // Inclusive Kogge-Stone scan of function composition (prefix then self).
-        Xfer inc = f;
+        // Inclusive Kogge-Stone scan of function composition (prefix then
+        // self): the prefix's exit offset picks this lane's entry, counts add.
+        // SCAN2: two shuffles a step on the packed words (fewer instructions,
+        // for the issue-bound single-point kernel); else four on the split
+        // fields (shorter dependent chain, for the latency-bound prefix
+        // kernel: 1 block per SM on config 2).
+        if (SCAN2) {
 #pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const int px0 = __shfl_up_sync(0xffffffffu, inc.x0, d);
-            const int px1 = __shfl_up_sync(0xffffffffu, inc.x1, d);
-            const int pc0 = __shfl_up_sync(0xffffffffu, inc.c0, d);
-            const int pc1 = __shfl_up_sync(0xffffffffu, inc.c1, d);
-            if (lane >= d) {
-                Xfer n;
-                n.x0 = px0 ? inc.x1 : inc.x0;
-                n.c0 = pc0 + (px0 ? inc.c1 : inc.c0);
-                n.x1 = px1 ? inc.x1 : inc.x0;
-                n.c1 = pc1 + (px1 ? inc.c1 : inc.c0);
-                inc = n;
+            for (int d = 1; d < 32; d <<= 1) {
+                const int p0 = __shfl_up_sync(0xffffffffu, e0, d);
+                const int p1 = __shfl_up_sync(0xffffffffu, e1, d);
+                if (lane >= d) {
+                    const int n0 = ((p0 & 1) ? e1 : e0) + (p0 & ~1);
+                    const int n1 = ((p1 & 1) ? e1 : e0) + (p1 & ~1);
+                    e0 = n0;
+                    e1 = n1;
+                }
             }
+        } else {
+            int x0 = e0 & 1, x1 = e1 & 1, c0 = e0 >> 1, c1 = e1 >> 1;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int px0 = __shfl_up_sync(0xffffffffu, x0, d);
+                const int px1 = __shfl_up_sync(0xffffffffu, x1, d);
+                const int pc0 = __shfl_up_sync(0xffffffffu, c0, d);
+                const int pc1 = __shfl_up_sync(0xffffffffu, c1, d);
+                if (lane >= d) {
+                    const int nx0 = px0 ? x1 : x0, nc0 = pc0 + (px0 ? c1 : c0);
+                    const int nx1 = px1 ? x1 : x0, nc1 = pc1 + (px1 ? c1 : c0);
+                    x0 = nx0;
+                    c0 = nc0;
+                    x1 = nx1;
+                    c1 = nc1;
+                }
+            }
+            e0 = x0 | (c0 << 1);
+            e1 = x1 | (c1 << 1);
         }
-        const int ex_x0 = __shfl_up_sync(0xffffffffu, inc.x0, 1);
-        const int ex_x1 = __shfl_up_sync(0xffffffffu, inc.x1, 1);
-        const int ex_c0 = __shfl_up_sync(0xffffffffu, inc.c0, 1);
-        const int ex_c1 = __shfl_up_sync(0xffffffffu, inc.c1, 1);
-        const int my_entry = lane == 0 ? entry : (entry ? ex_x1 : ex_x0);
-        int pos = lane == 0 ? 0 : (entry ? ex_c1 : ex_c0);
+        const int ex0 = __shfl_up_sync(0xffffffffu, e0, 1);
+        const int ex1 = __shfl_up_sync(0xffffffffu, e1, 1);
+        const int ex = entry ? ex1 : ex0;
+        const int my_entry = lane == 0 ? entry : (ex & 1);
+        int pos = lane == 0 ? 0 : (ex >> 1);
 
         // Emit this lane's values.
         if (carry_has) emit(pos++, carry_v);
@@ -149,8 +163,8 @@ __device__ __forceinline__ int64_t gen_stream(const ZigSmem* zs, int lane, const
                 }
         }
         // Chunk totals from lane 31; detect a carried attempt at word 127.
-        const int tot = __shfl_sync(0xffffffffu, entry ? inc.c1 : inc.c0, 31);
-        const int nxt = __shfl_sync(0xffffffffu, entry ? inc.x1 : inc.x0, 31);
+        const int last = __shfl_sync(0xffffffffu, entry ? e1 : e0, 31);
+        const int tot = last >> 1, nxt = last & 1;
         pend_w = __shfl_sync(0xffffffffu, w[3], 31);
         chunk_done(produced, tot);
         produced += tot;
@@ -170,6 +184,15 @@ constexpr int EXP_WARPS = 8;
 // The simulator's interleaved stream layout (jffc_seg.cu il4_off): stream r's
 // value i at (r / 32) * 32 * ld + (i / 4) * 128 + (r % 32) * 4 + i % 4.
 __device__ __forceinline__ int64_t il4_pos(int64_t i) { return ((i >> 2) << 7) + (i & 3); }
+
+// A chunk's values cv[0, tot) to stream positions produced.. of row o (IL4),
+// clipped at n_draws (> produced); value i + 32 lies 32 / 4 * 128 further.
+__device__ __forceinline__ void il4_write_chunk(double* __restrict__ o, const double* cv, int lane,
+                                                int64_t produced, int tot, int64_t n_draws) {
+    const int lim = n_draws - produced < tot ? (int)(n_draws - produced) : tot;
+    double* __restrict__ p = o + il4_pos(produced + lane);
+    for (int i = lane; i < lim; i += 32, p += 1024) *p = cv[i];
+}
 
 // IL4: the interleaved layout, each chunk written in order from a per-warp
 // buffer (4 consecutive lanes fill one 32-byte sector).
@@ -191,7 +214,7 @@ __global__ void __launch_bounds__(EXP_WARPS * 32, 2) exp_streams_kernel(const ui
     int64_t base = 0;
     ulonglong2* ks = sh_ks[threadIdx.x >> 5];
     philox_key_schedule(ks, lane, keys[2 * stream], keys[2 * stream + 1]);
-    gen_stream(
+    gen_stream<true>(
         &zs, lane, ks, n_draws, log1p_fma,
         [&](int i, double x) {
             if (IL4)
@@ -202,10 +225,7 @@ __global__ void __launch_bounds__(EXP_WARPS * 32, 2) exp_streams_kernel(const ui
         [&](int64_t produced, int tot) {
             if (IL4) {
                 __syncwarp();
-                for (int i = lane; i < tot; i += 32) {
-                    const int64_t q = produced + i;
-                    if (q < n_draws) o[il4_pos(q)] = cv[i];
-                }
+                il4_write_chunk(o, cv, lane, produced, tot, n_draws);
                 __syncwarp();
             }
             base = produced + tot;
@@ -320,7 +340,7 @@ __global__ void __launch_bounds__(W * 32, W == 16 ? 1 : 2) exp_streams_prefix_ke
     int64_t base = 0;
     ulonglong2* ks = sh_ks[threadIdx.x >> 5];
     philox_key_schedule(ks, lane, keys[2 * stream], keys[2 * stream + 1]);
-    gen_stream(
+    gen_stream<false>(
         &zs, lane, ks, n_draws, log1p_fma,
         [&](int i, double x) {
             cv[i] = x;
@@ -329,10 +349,7 @@ __global__ void __launch_bounds__(W * 32, W == 16 ? 1 : 2) exp_streams_prefix_ke
         [&](int64_t produced, int tot) {
             __syncwarp();
             if (IL4) {  // the chunk's values in order: 4-value sectors of this row
-                for (int i = lane; i < tot; i += 32) {
-                    const int64_t q = produced + i;
-                    if (q < n_draws) o[il4_pos(q)] = cv[i];
-                }
+                il4_write_chunk(o, cv, lane, produced, tot, n_draws);
             }
             if (produced < pp.n_cum) {
                 const int cnt = (int)min((int64_t)tot, pp.n_cum - produced);
