@@ -5,12 +5,13 @@
 // sizes are S[n:2n] of ONE stream S = standard_exponential(2n); the survey's
 // common-random-number identity).
 //
-// Layout: one warp per stream.  A chunk is 32 consecutive Philox blocks
-// (lane l owns block 32*c + l, i.e. counter 32*c + l + 1, words 4l..4l+3).
+// Layout: one warp per stream.  A chunk is 32 NB consecutive Philox blocks
+// (lane l owns blocks 32 NB c + NB l + b, b < NB, i.e. its NW = 4 NB words
+// are the chunk's words NW l .. NW l + NW - 1).
 // Every word is classified as the START of a ziggurat attempt (fast accept:
 // 1 word, value x; slow: 2 words, value or reject).  Whether a word actually
 // starts an attempt depends on all earlier words, but an attempt never spans
-// more than 2 words, so each lane's 4 words form a transfer function
+// more than 2 words, so each lane's NW words form a transfer function
 // {entry offset 0|1} -> {exit offset 0|1, values emitted}.  A 5-step warp
 // shuffle scan composes those functions, giving every lane its true entry
 // offset and output position.  A slow attempt starting at the chunk's last
@@ -27,59 +28,74 @@ namespace cs {
 // stream order) and then chunk_done(produced, tot) by every lane (produced =
 // the stream's values before this chunk, tot = this chunk's count; emitted
 // values may run past n_draws, the callbacks clip).
-template <bool SCAN2, typename Emit, typename Done>
+template <bool SCAN2, int NB, bool PIPE, typename Emit, typename Done>
 __device__ __forceinline__ int64_t gen_stream(const ZigSmem* zs, int lane, const ulonglong2* ks,
                                               int64_t n_draws, int log1p_fma, Emit&& emit, Done&& chunk_done) {
+    constexpr int NW = 4 * NB;  // words per lane per chunk (NB Philox blocks)
     int64_t produced = 0;
     int entry = 0;        // warp-uniform: offset of the first attempt in this chunk
     uint64_t pend_w = 0;  // word that started the carried slow attempt (entry == 1)
     uint64_t chunk = 0;
-    // software-pipelined: the next chunk's Philox blocks (a long dependent
-    // multiply chain per lane) are computed while this chunk is classified,
-    // scanned and emitted
-    uint64_t wn[4];
-    philox4x64_10_ks(lane + 1, ks, wn);
-    while (produced < n_draws) {
-        uint64_t w[4];
+    // PIPE: software-pipelined, the next chunk's Philox blocks (a long
+    // dependent multiply chain per lane) are computed while this chunk is
+    // classified, scanned and emitted
+    uint64_t wn[NW];
+    if (PIPE) {
 #pragma unroll
-        for (int q = 0; q < 4; q++) w[q] = wn[q];
-        philox4x64_10_ks((chunk + 1) * 32 + lane + 1, ks, wn);
+        for (int b = 0; b < NB; b++) philox4x64_10_ks(lane * NB + b + 1, ks, wn + 4 * b);
+    }
+    while (produced < n_draws) {
+        uint64_t w[NW];
+        if (PIPE) {
+#pragma unroll
+            for (int q = 0; q < NW; q++) w[q] = wn[q];
+#pragma unroll
+            for (int b = 0; b < NB; b++) philox4x64_10_ks((chunk + 1) * 32 * NB + lane * NB + b + 1, ks, wn + 4 * b);
+        } else {
+#pragma unroll
+            for (int b = 0; b < NB; b++) philox4x64_10_ks(chunk * 32 * NB + lane * NB + b + 1, ks, w + 4 * b);
+        }
         const uint64_t wnext = __shfl_down_sync(0xffffffffu, w[0], 1);
 
         // Per-word attempt results.
-        double v[4];
-        int adv[4];
-        bool has[4];
+        double v[NW];
+        int adv[NW];
+        bool has[NW];
         // Fast accepts first; a lane's slow attempts (about one word in 90:
         // 3/4 of the chunks have one somewhere in the warp) then run in ONE
         // loop, so a chunk pays the divergent slow path about once instead
-        // of once per word position.  Bit 4: the attempt carried from the
+        // of once per word position.  Bit 16: the attempt carried from the
         // previous chunk (lane 0, entry 1), resolved with this chunk's word 0.
-        unsigned slow = lane == 0 && entry == 1 ? 16u : 0u;
+        unsigned slow = lane == 0 && entry == 1 ? 1u << 16 : 0u;
 #pragma unroll
-        for (int p = 0; p < 4; p++) {
+        for (int p = 0; p < NW; p++) {
             double x;
             const bool f = zig_fast(zs, w[p], &x);
-            v[p] = f ? x : 0.0;  // a slow attempt at word 127 is carried
+            v[p] = f ? x : 0.0;  // a slow attempt at the chunk's last word is carried
             adv[p] = f ? 1 : 2;
             has[p] = f;
-            if (!f && (p < 3 || lane < 31)) slow |= 1u << p;
+            if (!f && (p < NW - 1 || lane < 31)) slow |= 1u << p;
         }
         bool carry_has = false;
         double carry_v = 0.0;
         while (slow) {
             const int p = __ffs(slow) - 1;
             slow &= slow - 1;
-            const uint64_t a = p == 0 ? w[0] : p == 1 ? w[1] : p == 2 ? w[2] : p == 3 ? w[3] : pend_w;
-            const uint64_t b = p == 0 ? w[1] : p == 1 ? w[2] : p == 2 ? w[3] : p == 3 ? wnext : w[0];
+            uint64_t a = pend_w, b = w[0];
+#pragma unroll
+            for (int q = 0; q < NW; q++)
+                if (p == q) {
+                    a = w[q];
+                    b = q < NW - 1 ? w[q + 1 < NW ? q + 1 : q] : wnext;
+                }
             const ZigAttempt r = zig_slow(zs, a, b, log1p_fma);
 #pragma unroll
-            for (int q = 0; q < 4; q++)
+            for (int q = 0; q < NW; q++)
                 if (p == q) {
                     v[q] = r.v;
                     has[q] = r.has;
                 }
-            if (p == 4) {
+            if (p == 16) {
                 carry_v = r.v;
                 carry_has = r.has;
             }
@@ -91,21 +107,21 @@ __device__ __forceinline__ int64_t gen_stream(const ZigSmem* zs, int lane, const
         {
             int p = 0, c = 0;
 #pragma unroll
-            for (int q = 0; q < 4; q++)
+            for (int q = 0; q < NW; q++)
                 if (p == q) {
                     c += has[q];
                     p += adv[q];
                 }
-            e0 = (p - 4) | (c << 1);
+            e0 = (p - NW) | (c << 1);
             p = 1;
             c = carry_has ? 1 : 0;
 #pragma unroll
-            for (int q = 1; q < 4; q++)
+            for (int q = 1; q < NW; q++)
                 if (p == q) {
                     c += has[q];
                     p += adv[q];
                 }
-            e1 = (p - 4) | (c << 1);
+            e1 = (p - NW) | (c << 1);
         }
         // Inclusive Kogge-Stone scan of function composition (prefix then
         // self): the prefix's exit offset picks this lane's entry, counts add.
@@ -156,16 +172,16 @@ __device__ __forceinline__ int64_t gen_stream(const ZigSmem* zs, int lane, const
         {
             int p = my_entry;
 #pragma unroll
-            for (int q = 0; q < 4; q++)
+            for (int q = 0; q < NW; q++)
                 if (p == q) {
                     if (has[q]) emit(pos++, v[q]);
                     p += adv[q];
                 }
         }
-        // Chunk totals from lane 31; detect a carried attempt at word 127.
+        // Chunk totals from lane 31; detect a carried attempt at the last word.
         const int last = __shfl_sync(0xffffffffu, entry ? e1 : e0, 31);
         const int tot = last >> 1, nxt = last & 1;
-        pend_w = __shfl_sync(0xffffffffu, w[3], 31);
+        pend_w = __shfl_sync(0xffffffffu, w[NW - 1], 31);
         chunk_done(produced, tot);
         produced += tot;
         entry = nxt;
@@ -180,6 +196,14 @@ __device__ __forceinline__ int64_t gen_stream(const ZigSmem* zs, int lane, const
 // took 134 -> one block per SM, config 5's 4096 streams in 4 waves instead of
 // 2: 119 -> 83 ms per chunk)
 constexpr int EXP_WARPS = 8;
+// Two Philox blocks (8 words) per lane per chunk, both computed at the top
+// of the chunk (two independent multiply chains): the per-chunk scan, slow
+// loop and write setup serve 256 words instead of 128.  Measured against one
+// block per lane with the next chunk's block software-pipelined: config 5
+// stream chunk 70.8 -> 61.2 ms, config 2 fused streams 3.15 -> 2.91 ms; two
+// blocks software-pipelined spill (64.1 ms), four spill heavily.
+constexpr int EXP_NB = 2, PFX_NB = 2;
+constexpr bool EXP_PIPE = false, PFX_PIPE = false;
 
 // The simulator's interleaved stream layout (jffc_seg.cu il4_off): stream r's
 // value i at (r / 32) * 32 * ld + (i / 4) * 128 + (r % 32) * 4 + i % 4.
@@ -202,7 +226,7 @@ __global__ void __launch_bounds__(EXP_WARPS * 32, 2) exp_streams_kernel(const ui
                                                                      double* __restrict__ out, int64_t ld,
                                                                      int log1p_fma) {
     __shared__ ZigSmem zs;
-    __shared__ double sh_vals[IL4 ? EXP_WARPS : 1][136];
+    __shared__ double sh_vals[IL4 ? EXP_WARPS : 1][128 * EXP_NB + 8];
     __shared__ ulonglong2 sh_ks[EXP_WARPS][10];
     zig_load(&zs);
     __syncthreads();
@@ -214,7 +238,7 @@ __global__ void __launch_bounds__(EXP_WARPS * 32, 2) exp_streams_kernel(const ui
     int64_t base = 0;
     ulonglong2* ks = sh_ks[threadIdx.x >> 5];
     philox_key_schedule(ks, lane, keys[2 * stream], keys[2 * stream + 1]);
-    gen_stream<true>(
+    gen_stream<true, EXP_NB, EXP_PIPE>(
         &zs, lane, ks, n_draws, log1p_fma,
         [&](int i, double x) {
             if (IL4)
@@ -322,7 +346,7 @@ __global__ void __launch_bounds__(W * 32, W == 16 ? 1 : 2) exp_streams_prefix_ke
     const uint64_t* __restrict__ keys, int64_t n_streams, int64_t n_draws, double* __restrict__ out,
     int64_t ld, int log1p_fma, const PrefixPlan pp) {
     __shared__ ZigSmem zs;
-    __shared__ double sh_vals[W][136];  // a chunk's values (<= 128 + carry), per warp
+    __shared__ double sh_vals[W][128 * PFX_NB + 8];  // a chunk's values (<= 128 NB + carry), per warp
     __shared__ ulonglong2 sh_ks[W][10];
     zig_load(&zs);
     __syncthreads();
@@ -340,7 +364,7 @@ __global__ void __launch_bounds__(W * 32, W == 16 ? 1 : 2) exp_streams_prefix_ke
     int64_t base = 0;
     ulonglong2* ks = sh_ks[threadIdx.x >> 5];
     philox_key_schedule(ks, lane, keys[2 * stream], keys[2 * stream + 1]);
-    gen_stream<false>(
+    gen_stream<false, PFX_NB, PFX_PIPE>(
         &zs, lane, ks, n_draws, log1p_fma,
         [&](int i, double x) {
             cv[i] = x;
