@@ -18,6 +18,12 @@
 //   [max(a_v, b_v + 1 - resid_v), b_v]: contiguous frontier buckets.
 //   Equal costs are broken by comparing the label paths through parent
 //   pointers (first differing node order from the head).
+//   Rounds after the first are incremental: a node's label is a function of
+//   its live predecessor set and those predecessors' labels, so only nodes
+//   whose live set shrank (the last chain's servers) or with a predecessor
+//   whose label (cost, path) changed are recomputed; the others keep theirs.
+//   Changed labels stamp their frontier bucket, and a node checks the stamps
+//   of its predecessor buckets.  Same labels as the full DP, far fewer scans.
 #include <cuda_runtime.h>
 #include <math.h>
 
@@ -213,6 +219,9 @@ __global__ void __launch_bounds__(512) gca_kernel(
     GcaNode* nd = reinterpret_cast<GcaNode*>(smem);
     int32_t* bucket = reinterpret_cast<int32_t*>(nd + max_nodes);  // nodes sorted by frontier
     int32_t* boff = bucket + max_nodes;                            // bucket offsets [0, L+3]
+    int32_t* dstamp = boff + max_levels + 1;   // [max_levels] round in which a bucket's label changed
+    int32_t* chstamp = dstamp + max_levels;    // [max_nodes] round in which a node's label changed
+    int32_t* rstamp = chstamp + max_nodes;     // [max_nodes] round whose live predecessor set shrank
     __shared__ int s_nodes, s_status, s_found, s_cap_fail;
     __shared__ unsigned long long s_edges;
     __shared__ int32_t s_path_len;
@@ -316,16 +325,21 @@ __global__ void __launch_bounds__(512) gca_kernel(
     }
     __syncthreads();
     const int64_t E = (int64_t)s_edges;
+    for (int v = tid; v < V; v += nthr) {
+        nd[v].cost = v == 0 ? 0.0 : INFINITY;
+        nd[v].parent = -1;
+        nd[v].depth = 0;
+        chstamp[v] = -1;
+        rstamp[v] = -1;
+    }
+    for (int f = tid; f < max_levels; f += nthr) dstamp[f] = -1;
+    __syncthreads();
     int K = 0;
     int64_t it = 0;
     for (it = 0; it <= E; it++) {
-        // --- DP labels in frontier order ---
-        for (int v = tid; v < V; v += nthr) {
-            nd[v].cost = v == 0 ? 0.0 : INFINITY;
-            nd[v].parent = -1;
-            nd[v].depth = 0;
-        }
-        __syncthreads();
+        const int32_t its = (int32_t)it;
+        // --- DP labels in frontier order (round 0: every node; later rounds:
+        //     the nodes whose live set or some predecessor's label changed) ---
         for (int F = 2; F <= L + 2; F++) {
             const int nb = boff[F + 1] - boff[F];
             for (int q = warp; q < nb; q += nwarps) {
@@ -337,6 +351,17 @@ __global__ void __launch_bounds__(512) gca_kernel(
                     if (need > lo) lo = need > (int64_t)(L + 3) ? L + 3 : (int)need;
                 }
                 const int hi = nv.rb;
+                if (its > 0 && rstamp[v] != its) {
+                    bool dirty = false;
+                    for (int f0 = lo; f0 <= hi; f0 += 32) {
+                        const int f = f0 + lane;
+                        if (__any_sync(0xffffffffu, f <= hi && dstamp[f] == its)) {
+                            dirty = true;
+                            break;
+                        }
+                    }
+                    if (!dirty) continue;  // same live set, same predecessor labels
+                }
                 double best = INFINITY;
                 int bu = -1;
                 if (lo <= hi) {
@@ -364,10 +389,16 @@ __global__ void __launch_bounds__(512) gca_kernel(
                         bu = ou;
                     }
                 }
-                if (lane == 0 && bu >= 0) {
-                    nd[v].cost = best;
-                    nd[v].parent = bu;
-                    nd[v].depth = nd[bu].depth + 1;
+                if (lane == 0) {
+                    const int op = nd[v].parent;
+                    const bool changed = bu != op || (bu >= 0 && (best != nd[v].cost || chstamp[bu] == its));
+                    if (changed) {
+                        nd[v].cost = bu >= 0 ? best : INFINITY;
+                        nd[v].parent = bu;
+                        nd[v].depth = bu >= 0 ? nd[bu].depth + 1 : 0;
+                        chstamp[v] = its;
+                        dstamp[nv.fr] = its;
+                    }
                 }
             }
             __syncthreads();
@@ -405,6 +436,7 @@ __global__ void __launch_bounds__(512) gca_kernel(
                         const int64_t m = (int64_t)nd[w].rb + 1 - nd[u].fr;
                         T.add(__dadd_rn(nd[w].tc, __dmul_rn(nd[w].tp, (double)m)));
                         nd[w].resid -= m * cap;
+                        rstamp[w] = (int32_t)(it + 1);  // live predecessor set shrinks next round
                         out[h] = nd[w].srv;
                         u = w;
                     }
@@ -469,7 +501,8 @@ extern "C" int cs_gca_batch_impl(const cs_compose_point* d_points, int32_t n_poi
     if (n_points <= 0) return CS_OK;
     const int max_nodes = max_servers + 2;
     const int max_levels = max_blocks_L + 4;
-    const size_t smem = sizeof(GcaNode) * max_nodes + sizeof(int32_t) * (max_nodes + max_levels + 1);
+    const size_t smem = sizeof(GcaNode) * max_nodes + sizeof(int32_t) * (max_nodes + max_levels + 1) +
+                        sizeof(int32_t) * (max_levels + 2 * (size_t)max_nodes);
     if (smem > 220 * 1024) {
         set_error("cs_gca_batch: %d servers per point exceeds shared memory", max_servers);
         return CS_UNSUPPORTED;

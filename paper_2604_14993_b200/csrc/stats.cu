@@ -134,31 +134,29 @@ __device__ __forceinline__ void cand_open(CandChunks& c, int lane, int nl, unsig
 }
 
 // Append w to local list ql (every lane calls it; ql < 0: nothing) -- the
-// part for list q; the caller loops q over the lists.
+// part for list q; the caller loops q over the lists.  Only warp-uniform
+// branches: a divergent branch makes the compiler wait for every load in
+// flight (the row pass keeps the next leaf group's loads in flight across
+// the appends).  cap_q / dst_q: list q's capacity and storage.
 __device__ __forceinline__ void cand_push(CandChunks& c, int lane, int q, int ql, double w,
-                                          unsigned long long* __restrict__ fill_g,
-                                          const int64_t* __restrict__ cap_g, const int64_t* __restrict__ off_g,
-                                          double* __restrict__ cand) {
+                                          unsigned long long* __restrict__ fill_g, unsigned long long cap_q,
+                                          double* __restrict__ dst_q) {
     const unsigned msk = __ballot_sync(0xffffffffu, ql == q);
     if (msk == 0) return;
     const int cnt = __popc(msk);
     const int u = __shfl_sync(0xffffffffu, c.used, q);
     const unsigned long long b = __shfl_sync(0xffffffffu, c.base, q);
+    const unsigned long long nb = __shfl_sync(0xffffffffu, c.next, q);
     const int pos = u + __popc(msk & ((1u << lane) - 1u));
-    unsigned long long slot = b + (unsigned long long)pos;
-    if (u + cnt > CAND_CHUNK) {  // this append crosses into the next reservation
-        const unsigned long long nb = __shfl_sync(0xffffffffu, c.next, q);
-        if (pos >= CAND_CHUNK) slot = nb + (unsigned long long)(pos - CAND_CHUNK);
-        if (lane == q) {
-            c.base = nb;
-            c.used = u + cnt - CAND_CHUNK;
-            c.next = atomicAdd(&fill_g[q], (unsigned long long)CAND_CHUNK);
-        }
-    } else if (lane == q) {
-        c.used = u + cnt;
-    }
-    if (lane == q) c.in += (uint32_t)cnt;
-    if (ql == q && slot < (unsigned long long)cap_g[q]) cand[off_g[q] + slot] = w;  // overflow: host check
+    const bool cross = u + cnt > CAND_CHUNK;  // this append crosses into the next reservation
+    const unsigned long long slot =
+        pos >= CAND_CHUNK ? nb + (unsigned long long)(pos - CAND_CHUNK) : b + (unsigned long long)pos;
+    const bool own = lane == q;
+    c.used = own ? (cross ? u + cnt - CAND_CHUNK : u + cnt) : c.used;
+    c.base = (own && cross) ? nb : c.base;
+    c.in += own ? (uint32_t)cnt : 0u;
+    if (own && cross) c.next = atomicAdd(&fill_g[q], (unsigned long long)CAND_CHUNK);
+    if (ql == q && slot < cap_q) dst_q[slot] = w;  // overflow: host check
 }
 
 // Seal the reservations: the current one's tail and the untouched next one.
@@ -214,7 +212,10 @@ __global__ void __launch_bounds__(256) compact_bucket_kernel(
                 }
                 // only the lists some lane appends to (usually one)
                 for (unsigned m = __reduce_or_sync(0xffffffffu, ql >= 0 ? 1u << ql : 0u); m; m &= m - 1)
-                    cand_push(cc, lane, __ffs(m) - 1, ql, v[k], fill + gl0, cap + gl0, off + gl0, cand);
+                {
+                    const int q = __ffs(m) - 1;
+                    cand_push(cc, lane, q, ql, v[k], fill + gl0, (unsigned long long)cap[gl0 + q], cand + off[gl0 + q]);
+                }
             }
         }
     }
@@ -233,6 +234,28 @@ __device__ __forceinline__ double pick_slot(const double (&v)[T], int t) {
 #pragma unroll
     for (int i = 0; i < 2; i++) l3[i] = (t & 4) ? l2[2 * i + 1] : l2[2 * i];
     return (t & 8) ? l3[1] : l3[0];
+}
+
+// bit if d[q] <= wid[q] for some q, else 0: one predicate chained through
+// the compares (setp .or), one select
+template <int NB>
+__device__ __forceinline__ uint32_t near_bit(const uint32_t (&d)[NB], const uint32_t (&wid)[NB], uint32_t bit) {
+    uint32_t r;
+    if (NB == 3) {
+        asm("{\n\t.reg .pred p;\n\t"
+            "setp.le.u32 p, %1, %2;\n\t"
+            "setp.le.or.u32 p, %3, %4, p;\n\t"
+            "setp.le.or.u32 p, %5, %6, p;\n\t"
+            "selp.b32 %0, %7, 0, p;\n\t}"
+            : "=r"(r)
+            : "r"(d[0]), "r"(wid[0]), "r"(d[1 % NB]), "r"(wid[1 % NB]), "r"(d[2 % NB]), "r"(wid[2 % NB]), "r"(bit));
+    } else {
+        bool nr = false;
+#pragma unroll
+        for (int q = 0; q < NB; q++) nr |= d[q] <= wid[q];
+        r = nr ? bit : 0u;
+    }
+    return r;
 }
 
 // Bracket state of one row (registers only: fixed sizes, static indices).
@@ -271,6 +294,11 @@ __device__ __forceinline__ int classify_one(Brackets<NB>& br, uint64_t u, bool h
 // optional bracket counting/compaction.  The plan (leaf offsets, lengths,
 // height-ordered nodes) sits in shared memory.
 constexpr int LB_WARPS = 8;
+// Per-lane staging of the values inside a bracket: appended with predicated
+// shared-memory stores (no branch: a divergent branch or a warp collective
+// inside a loop makes the compiler wait for the next leaf group's loads, which
+// the pass keeps in flight), handed to the candidate lists when some lane
+// could overflow in the next group, and at the row's end.
 
 // T = value slots per lane and leaf: 8*T >= the plan's longest leaf (numpy
 // leaves hold 64..128 values; 90000-value rows have 80/88-value leaves, so
@@ -283,14 +311,17 @@ __global__ void __launch_bounds__(LB_WARPS * 32, 2) row_stats_kernel(
     const uint64_t* __restrict__ lo, const uint64_t* __restrict__ hi, const int64_t* __restrict__ off,
     const int64_t* __restrict__ cap, unsigned long long* __restrict__ fill,
     unsigned long long* __restrict__ below, unsigned long long* __restrict__ inside,
-    double* __restrict__ cand, int32_t n_heights, double* __restrict__ leaf_scratch) {
+    double* __restrict__ cand, int32_t n_heights, double* __restrict__ leaf_scratch, int32_t stg_slots) {
     // shared: per-warp leaf values [LB_WARPS][L] doubles, then the plan:
     // leaf offset[L], leaf length[L], height offsets[n_heights + 1] and the
     // internal nodes in height order as (a, b) pairs: v[a] = v[a] + v[b]
     // (a = the node's leftmost leaf, b = its right child's leftmost leaf)
     // leaf values: shared memory, or (long rows) a global scratch slice per warp
     extern __shared__ double row_sh[];
-    int32_t* plan = reinterpret_cast<int32_t*>(leaf_scratch ? row_sh : row_sh + (size_t)LB_WARPS * L);
+    const int STG = stg_slots;  // >= T + 3
+    double* stage_sh = row_sh;  // [LB_WARPS][STG][32]
+    double* leaf_sh = row_sh + (size_t)LB_WARPS * STG * 32;
+    int32_t* plan = reinterpret_cast<int32_t*>(leaf_scratch ? leaf_sh : leaf_sh + (size_t)LB_WARPS * L);
     const int plan_words = 2 * L + (n_heights + 1) + 2 * (L - 1);
     for (int q = threadIdx.x; q < plan_words; q += blockDim.x) plan[q] = g_plan[q];
     __syncthreads();
@@ -300,8 +331,9 @@ __global__ void __launch_bounds__(LB_WARPS * 32, 2) row_stats_kernel(
     const int32_t* nodes = h_off + n_heights + 1;
     double* lv = leaf_scratch
                      ? leaf_scratch + ((size_t)blockIdx.x * LB_WARPS + (threadIdx.x >> 5)) * (size_t)L
-                     : row_sh + (size_t)(threadIdx.x >> 5) * L;
+                     : leaf_sh + (size_t)(threadIdx.x >> 5) * L;
     const int lane = threadIdx.x & 31, j = lane & 7, sub = lane >> 3, warp = threadIdx.x >> 5;
+    double* const stg = stage_sh + (size_t)warp * STG * 32 + lane;  // slot i at stg[32 * i]
     for (int64_t row = (int64_t)blockIdx.x * LB_WARPS + warp; row < n_rows; row += (int64_t)gridDim.x * LB_WARPS) {
         const int64_t g = row / rows_per_group;
         const int nl = do_bracket ? grp_nlist[g] : 0;  // warp-uniform, <= NB (checked on the host)
@@ -317,11 +349,71 @@ __global__ void __launch_bounds__(LB_WARPS * 32, 2) row_stats_kernel(
         }
         const double* __restrict__ rowp = resp + row * ldr;
         const int64_t gl0 = g * MAX_LISTS;
-        CandChunks cc{0ull, 0ull, 0, 0u};
-        if (do_bracket) cand_open(cc, lane, nl, fill + gl0);
-        auto push = [&](int ql, double w) {  // every lane; ql = local list or -1
+        unsigned long long capq[NB];
+        double* dstq[NB];
 #pragma unroll
-            for (int q = 0; q < NB; q++) cand_push(cc, lane, q, ql, w, fill + gl0, cap + gl0, off + gl0, cand);
+        for (int q = 0; q < NB; q++) {
+            capq[q] = q < nl ? (unsigned long long)cap[gl0 + q] : 0ull;
+            dstq[q] = q < nl ? cand + off[gl0 + q] : cand;
+        }
+        auto list_of = [&](double w) {  // bracket list of an inside value
+            const uint32_t hw = (uint32_t)(dbits(w) >> 32);
+            int ql = 0;
+#pragma unroll
+            for (int q = 1; q < NB; q++) ql = hw - br.lo_hw[q] <= br.wid_hw[q] ? q : ql;
+            return ql;
+        };
+        // Hand the staged values to the candidate lists: per list a warp scan
+        // of the lanes' counts and one exact reservation (atomicAdd by lane
+        // 31), then every lane stores its values at its offsets.
+        uint32_t ns = 0;  // this lane's staged values
+        auto drain_stage = [&]() {
+            const int nmax = (int)__reduce_max_sync(0xffffffffu, ns);
+            if (nmax == 0) return;
+            uint32_t cq[NB];
+#pragma unroll
+            for (int q = 0; q < NB; q++) cq[q] = 0;
+            for (int i = 0; i < nmax; i++) {
+                const int ql = (uint32_t)i < ns ? list_of(stg[32 * i]) : -1;
+#pragma unroll
+                for (int q = 0; q < NB; q++) cq[q] += ql == q ? 1u : 0u;
+            }
+            unsigned long long pos[NB];
+#pragma unroll
+            for (int q = 0; q < NB; q++) {
+                uint32_t inc = cq[q];
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+                    if (lane >= d) inc += o;
+                }
+                const uint32_t tot = __shfl_sync(0xffffffffu, inc, 31);
+                unsigned long long base = 0;
+                if (lane == 31 && tot) {
+                    base = atomicAdd(&fill[gl0 + q], (unsigned long long)tot);
+                    atomicAdd(&inside[gl0 + q], (unsigned long long)tot);
+                }
+                pos[q] = __shfl_sync(0xffffffffu, base, 31) + (inc - cq[q]);
+            }
+            for (int i = 0; i < nmax; i++) {
+                if ((uint32_t)i < ns) {
+                    const double w = stg[32 * i];
+                    const int ql = list_of(w);
+#pragma unroll
+                    for (int q = 0; q < NB; q++)
+                        if (ql == q) {
+                            if (pos[q] < capq[q]) dstq[q][pos[q]] = w;  // overflow: host check
+                            pos[q]++;
+                        }
+                }
+            }
+            ns = 0;
+        };
+        auto stage = [&](bool p, double w) {  // predicated, no branch
+            if (p) {
+                stg[32 * ns] = w;
+                ns++;
+            }
         };
         // Software pipeline: the next leaf group's loads are in flight while
         // this group is summed and classified.
@@ -352,35 +444,19 @@ __global__ void __launch_bounds__(LB_WARPS * 32, 2) row_stats_kernel(
                 // word decides: d = hw - lo_hw, "below" is its sign (all high
                 // words < 2^31) and "inside" is d <= wid
                 npad += (uint32_t)(T - nvalid);
-                uint32_t nearm = 0;
 #pragma unroll
                 for (int t = 0; t < T; t++) {
                     const uint32_t hw = (uint32_t)(dbits(v[t]) >> 32);
-                    bool nr = false;
+                    uint32_t d[NB];
 #pragma unroll
                     for (int q = 0; q < NB; q++) {
-                        const uint32_t d = hw - br.lo_hw[q];
-                        br.cnt[q] += d >> 31;
-                        nr |= d <= br.wid_hw[q];
+                        d[q] = hw - br.lo_hw[q];
+                        br.cnt[q] += d[q] >> 31;
                     }
-                    if (nr) nearm |= 1u << t;
+                    // a pad (+0.0, slot >= nvalid) is inside a bracket starting at 0
+                    stage(near_bit<NB>(d, br.wid_hw, 1u) && t < nvalid, v[t]);
                 }
-                nearm &= (1u << nvalid) - 1u;  // a pad (+0.0) is inside a bracket starting at 0
-                // the (few) values inside a bracket, appended
-                while (__any_sync(0xffffffffu, nearm != 0)) {
-                    int ql = -1;
-                    double w = 0.0;
-                    if (nearm) {
-                        const int t = __ffs(nearm) - 1;
-                        nearm &= nearm - 1;
-                        w = pick_slot<T>(v, t);
-                        const uint32_t hw = (uint32_t)(dbits(w) >> 32);
-#pragma unroll
-                        for (int q = 0; q < NB; q++)
-                            if (hw - br.lo_hw[q] <= br.wid_hw[q]) ql = q;
-                    }
-                    push(ql, w);
-                }
+                if (__any_sync(0xffffffffu, ns > (uint32_t)(STG - T))) drain_stage();
             }
             // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) in numpy's order
             const double s1 = __dadd_rn(acc, __shfl_down_sync(0xffffffffu, acc, 1));
@@ -396,7 +472,8 @@ __global__ void __launch_bounds__(LB_WARPS * 32, 2) row_stats_kernel(
                 const double w = have ? a[idx] : 0.0;
                 if (have) res = __dadd_rn(res, w);
                 if (do_bracket) {
-                    push(classify_one<NB>(br, dbits(w), have), w);
+                    stage(classify_one<NB>(br, dbits(w), have) >= 0, w);
+                    if (__any_sync(0xffffffffu, ns >= (uint32_t)STG)) drain_stage();
                 }
             }
             if (j == 0 && valid) lv[leaf] = res;  // leaves l0..l0+3 (lanes 0, 8, 16, 24)
@@ -411,6 +488,7 @@ __global__ void __launch_bounds__(LB_WARPS * 32, 2) row_stats_kernel(
             process_group(l0, v);
         }
         if (do_bracket) {
+            drain_stage();
 #pragma unroll
             for (int q = 0; q < NB; q++) br.cnt[q] -= ((0u - br.lo_hw[q]) >> 31) * npad;
         }
@@ -439,8 +517,7 @@ __global__ void __launch_bounds__(LB_WARPS * 32, 2) row_stats_kernel(
                 for (int d = 16; d > 0; d >>= 1) c += __shfl_down_sync(0xffffffffu, c, d);
                 if (lane == 0 && q < nl && c) atomicAdd(&below[g * MAX_LISTS + q], (unsigned long long)c);
             }
-            cand_seal(cc, lane, nl, cap + gl0, off + gl0, cand);
-            if (lane < nl && cc.in) atomicAdd(&inside[gl0 + lane], (unsigned long long)cc.in);
+
         }
     }
 }
@@ -769,9 +846,20 @@ extern "C" int cs_rep_stats_impl(const double* d_resp, int32_t n_groups, int64_t
     const int32_t n_heights = (int32_t)pl.by_height.size();
     const size_t plan_words = 2 * (size_t)L + n_heights + 1 + 2 * (size_t)std::max(L - 1, 0);
     const size_t plan_bytes = sizeof(int32_t) * plan_words;
-    const bool leaves_in_smem = sizeof(double) * LB_WARPS * (size_t)L + plan_bytes <= 160 * 1024;
-    const size_t smem = (leaves_in_smem ? sizeof(double) * LB_WARPS * (size_t)L : 0) + plan_bytes;
-    if (smem > 200 * 1024) {
+    const int max_leaf = pl.leaf_len.empty() ? 0 : *std::max_element(pl.leaf_len.begin(), pl.leaf_len.end());
+    const bool slots12 = max_leaf <= 96;  // 8 lanes x 12 slots cover every leaf's 8-aligned body
+    const int t_slots = slots12 ? 12 : 16;
+    // shared memory: the inside-value staging ring ([LB_WARPS][stg][32] doubles;
+    // a deep ring keeps its hand-overs rare), the leaf sums when they fit
+    // beside it with two blocks per SM (else a global scratch slice per
+    // warp, L2-resident), the plan
+    auto stage_bytes = [&](int stg) { return sizeof(double) * LB_WARPS * 32 * (size_t)stg; };
+    const size_t lv_bytes = sizeof(double) * LB_WARPS * (size_t)L;
+    const bool leaves_in_smem = stage_bytes(t_slots + 28) + lv_bytes + plan_bytes <= 110 * 1024;
+    int stg = t_slots + 28;
+    while (stg > t_slots + 3 && stage_bytes(stg) + (leaves_in_smem ? lv_bytes : 0) + plan_bytes > 224 * 1024) stg--;
+    const size_t smem = stage_bytes(stg) + (leaves_in_smem ? lv_bytes : 0) + plan_bytes;
+    if (smem > 224 * 1024) {
         set_error("cs_rep_stats: rows of %lld responses exceed the on-chip pairwise plan", (long long)m);
         return CS_UNSUPPORTED;
     }
@@ -791,8 +879,6 @@ extern "C" int cs_rep_stats_impl(const double* d_resp, int32_t n_groups, int64_t
         cudaMemcpyAsync(b_plan.p, h.data(), sizeof(int32_t) * h.size(), cudaMemcpyHostToDevice, st);
         if ((rc = check_cuda(cudaStreamSynchronize(st), "plan upload"))) return rc;  // h dies here
     }
-    const int max_leaf = pl.leaf_len.empty() ? 0 : *std::max_element(pl.leaf_len.begin(), pl.leaf_len.end());
-    const bool slots12 = max_leaf <= 96;  // 8 lanes x 12 slots cover every leaf's 8-aligned body
     for (auto k : {row_stats_kernel<3, 12>, row_stats_kernel<3, 16>, row_stats_kernel<MAX_LISTS, 12>,
                    row_stats_kernel<MAX_LISTS, 16>})
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 16));
@@ -810,7 +896,7 @@ extern "C" int cs_rep_stats_impl(const double* d_resp, int32_t n_groups, int64_t
                                    : (slots12 ? row_stats_kernel<MAX_LISTS, 12> : row_stats_kernel<MAX_LISTS, 16>);
         k<<<blocks, LB_WARPS * 32, std::max<size_t>(smem, 16), st>>>(
             d_resp, n_rows, rows_per_group, ldr, m, b_plan.as<int32_t>(), L, d_summ, d_row_sums, do_bracket,
-            nl, lo, hi, off, cap, fill, below, inside, cand, n_heights, leaf_scratch);
+            nl, lo, hi, off, cap, fill, below, inside, cand, n_heights, leaf_scratch, stg);
         return check_launch("row_stats_kernel");
     };
     const RowView full{m, 40, 40};  // contiguous
