@@ -508,7 +508,7 @@ def main():
     c5 = None if args.no_config5 else config5(P, rates, caps, nu, rank, world, barrier, torch)
     comp = None
     if rank == 0 and world == 1 and not args.no_compose:
-        comp = compose_config4(10_000, 256, 3)
+        comp = compose_config4(10_000, 10_000, 3)
 
     if rank == 0:
         cpu = None if args.no_cpu_baseline or world > 1 else cpu_baseline(rates, caps, lams, args)

@@ -62,28 +62,32 @@ constexpr int AG_WAIT = 0, AG_SERV = 1, AG_AMID = 2, AG_AEND = 3, AG_BUSY = 4, A
 // finalize kernel -- one fixed association for a given n, whatever the
 // segment count, the batch shape or the GPU count
 constexpr int64_t BS = 256;
-constexpr int MAXQ = 20;
+#ifndef CS_SEG_MAXQ
+#define CS_SEG_MAXQ 28
+#endif
+constexpr int MAXQ = CS_SEG_MAXQ;
 constexpr uint32_t DONE = 1u << 30;
 constexpr int32_t ST_UNKNOWN = 0, ST_SKIPPED = 1;  // status >= 2: EXACT, coupled at job (status - 2)
 
 // checkpoint offsets from a segment's first job, in blocks: dense first
 // (typical coupling within 32-300 jobs), sparser for the rho -> 1 tails
 __host__ __device__ inline int64_t ck_offset(int q) {
-    // 1..8, 10..16 step 2, 20..32 step 4, 40..64 step 8 blocks
-    const int m = q <= 8 ? q : q <= 12 ? 2 * q - 8 : q <= 16 ? 4 * q - 32 : 8 * q - 96;
+    // 1..8, 10..16 step 2, 20..32 step 4, 40..64 step 8, 80..192 step 16 blocks
+    const int m = q <= 8 ? q : q <= 12 ? 2 * q - 8 : q <= 16 ? 4 * q - 32 : q <= 20 ? 8 * q - 96 : 16 * q - 256;
     return BS * m;
 }
 
-// Segment lengths grow linearly with the segment index: segment s gets a
+// Segment lengths may grow linearly with the segment index: segment s gets a
 // share (1 + k (2s - S + 1) / (S - 1)) / S of the row, k = -CS_SEG_SKEW/1000.
-// The warp schedulers favour older warps, and the blocks of the early
-// segments are launched first, so the early segments run ahead; shorter
-// early segments end their phase 1 when the later ones do and start the
-// hand-over chain earlier.  Measured (kernel, config 2 / config-5 chunk of
-// 2048 reps): skew 0 10.99 / 17.60 ms, -100 10.12 / 16.87, -150 10.35 /
-// 16.53, -200 10.52 / 16.73, -250 10.81 / 17.00.  Results do not depend on it.
+// With single-warp blocks spread over all SMs the early segments ran ahead
+// (older warps, launched first) and shorter early segments helped (kernel,
+// config 2 / config-5 chunk of 2048 reps: skew 0 10.99 / 17.60 ms, -100
+// 10.12 / 16.87, -150 10.35 / 16.53).  With whole-SM blocks (every scheduler
+// holding 4 consecutive segments of one row group) equal segments are best:
+// config 2 kernel / pipelined step, skew -100 10.36 / 15.51 ms, 0 10.15 /
+// 15.32, +50 10.50 / 15.61, +100 10.33 / 15.52.  Results do not depend on it.
 #ifndef CS_SEG_SKEW
-#define CS_SEG_SKEW (-100)  // per mille
+#define CS_SEG_SKEW 0  // per mille
 #endif
 __host__ __device__ inline int64_t seg_begin(int s, int S, int64_t n) {
     if (s <= 0) return 0;
@@ -301,9 +305,6 @@ enum { PH_A = 0, PH_B = 1, PH_C = 2 };  // before warm-up / first / second half 
 
 // <= 128 registers: 16 warps per SM (measured against 20 and 24 warps with
 // spills: 13.6 / 14.7 / 17.8 ms on config 2; without the bound ptxas took 144)
-#ifndef CS_SEG_MINB
-#define CS_SEG_MINB 16
-#endif
 #ifndef CS_SEG_UNROLL
 #define CS_SEG_UNROLL 4  // measured on config 2: 1 11.77, 2 11.83, 4 11.10 ms
 #endif
@@ -318,8 +319,25 @@ constexpr int SEG_UNROLL = CS_SEG_UNROLL;  // jobs per trip of the step loops
 // so a warp's step reads 8 lines, each consumed within 4 steps.
 __device__ __forceinline__ int64_t il4_off(int64_t i) { return ((i >> 2) << 7) + (i & 3); }
 
+// One warp's shared memory (a block holds SEG_WPB of them).
+template <int CMAX>
+struct SegSmem {
+    double ring[32 * 33];  // response ring: element (pos, lane) at [pos & 31][lane], row pitch 33 doubles
+    double rbuf[CMAX * 32];  // response of the job holding slot id
+    double* row[32];         // response row of each lane
+    int4 meta[32];           // per-lane flush line: start, first, end, has
+};
+
+// Blocks of SEG_WPB warps (one block fills an SM's register file at 128
+// registers): a launch of U units occupies ceil(U / 16) whole SMs, every
+// scheduler holding 4 units -- 4 consecutive segments of one row group when
+// S = 4 -- instead of U single-warp blocks spread 3 or 4 to a scheduler over
+// all SMs (the kernel ends with the 4-warp schedulers either way; the SMs it
+// does not need stay free for the next sweep's streams).
+constexpr int SEG_WPB = 16;
+
 template <int CMAX, bool IL4>
-__global__ void __launch_bounds__(32, CS_SEG_MINB) jffc_seg_kernel(Args A) {
+__global__ void __launch_bounds__(32 * SEG_WPB, 1) jffc_seg_kernel(Args A) {
     constexpr int ID_BITS = CMAX <= 8 ? 3 : 4;
     constexpr uint32_t DUMMY = 0x80000000u;  // an initially idle slot, not a job
     constexpr uint32_t J_MASK = (1u << (31 - ID_BITS)) - 1;
@@ -327,15 +345,20 @@ __global__ void __launch_bounds__(32, CS_SEG_MINB) jffc_seg_kernel(Args A) {
     constexpr int FCK = CMAX + 1;
     constexpr unsigned FULL = 0xffffffffu;
 
-    // response ring: element (pos, lane) at [pos & 31][lane], row pitch 33 doubles
-    __shared__ __align__(16) double sh_ring[32 * 33];
-    __shared__ double sh_rbuf[CMAX * 32];  // response of the job holding slot id
-    __shared__ double* sh_row[32];         // response row of each lane
-    __shared__ int4 sh_meta[32];           // per-lane flush line: start, first, end, has
+    extern __shared__ __align__(16) unsigned char seg_smem[];
+    const int wib = threadIdx.x >> 5;
+    SegSmem<CMAX>& wsm = reinterpret_cast<SegSmem<CMAX>*>(seg_smem)[wib];
+    double* const sh_ring = wsm.ring;
+    double* const sh_rbuf = wsm.rbuf;
+    double** const sh_row = wsm.row;
+    int4* const sh_meta = wsm.meta;
 
-    const int lane = threadIdx.x;
+    const int lane = threadIdx.x & 31;
     const int S = A.nseg, G = A.G, Q = A.Q;
-    const int s = blockIdx.x / G, g = blockIdx.x % G;
+    // scheduler z = 4 * block + (warp & 3) hosts units 4z .. 4z + 3 (unit = g * S + s)
+    const int64_t uo = ((int64_t)blockIdx.x * 4 + (wib & 3)) * 4 + (wib >> 2);
+    if (uo >= (int64_t)S * G) return;
+    const int s = (int)(uo % S), g = (int)(uo / S);
     const int64_t T = (int64_t)A.P * A.R;
     const int64_t tid = (int64_t)g * 32 + lane;
     const bool valid = tid < T;
@@ -358,7 +381,7 @@ __global__ void __launch_bounds__(32, CS_SEG_MINB) jffc_seg_kernel(Args A) {
 
     const int64_t b = seg_begin(s, S, n), e = seg_begin(s + 1, S, n);
     const int unit = s * G + g;
-    unsigned long long* tr = A.trace ? A.trace + (int64_t)blockIdx.x * 4 : nullptr;
+    unsigned long long* tr = A.trace ? A.trace + (int64_t)unit * 4 : nullptr;
     if (tr && lane == 0) tr[0] = gtimer();
 
     // ---- lane state
@@ -787,12 +810,16 @@ static int max_resident_blocks() {
     if (cudaGetDevice(&dev) != cudaSuccess) return 0;
     if (dev < 64 && cached[dev]) return cached[dev];
     int per_sm = 0, sms = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jffc_seg_kernel<CMAX, IL4>, 32, 0) != cudaSuccess ||
+    const int smem = (int)(sizeof(SegSmem<CMAX>) * SEG_WPB);
+    if (cudaFuncSetAttribute(jffc_seg_kernel<CMAX, IL4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
+            cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jffc_seg_kernel<CMAX, IL4>, 32 * SEG_WPB, smem) !=
+            cudaSuccess ||
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
         cudaGetLastError();
         return 0;
     }
-    const int v = per_sm * sms;
+    const int v = per_sm * SEG_WPB * sms;  // resident units (warps)
     if (dev < 64) cached[dev] = v;
     return v;
 }
@@ -846,11 +873,14 @@ static Plan make_plan(int32_t P, int32_t R, int32_t max_cap, int64_t n) {
 
 template <int CMAX, bool IL4>
 static int launch(const Plan& pl, Args A, cudaStream_t st) {
-    const int blocks = pl.S * pl.G;
+    const int units = pl.S * pl.G;
+    const int blocks = (units + SEG_WPB - 1) / SEG_WPB;
+    const size_t smem = sizeof(SegSmem<CMAX>) * SEG_WPB;
+    cudaFuncSetAttribute(jffc_seg_kernel<CMAX, IL4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const bool trace = getenv("CS_SEG_TRACE") != nullptr;  // development timeline (stderr)
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     if (trace) {
-        cudaMalloc(&A.trace, sizeof(unsigned long long) * 4 * blocks);
+        cudaMalloc(&A.trace, sizeof(unsigned long long) * 4 * units);
         cudaEventCreate(&ev0);
         cudaEventCreate(&ev1);
         cudaEventRecord(ev0, st);
@@ -858,10 +888,11 @@ static int launch(const Plan& pl, Args A, cudaStream_t st) {
     if (pl.S > 1) {  // phase-2 waits need every segment resident
         void* params[] = {&A};
         const cudaError_t e =
-            cudaLaunchCooperativeKernel((const void*)jffc_seg_kernel<CMAX, IL4>, dim3(blocks), dim3(32), params, 0, st);
+            cudaLaunchCooperativeKernel((const void*)jffc_seg_kernel<CMAX, IL4>, dim3(blocks), dim3(32 * SEG_WPB),
+                                        params, smem, st);
         if (e != cudaSuccess) return check_cuda(e, "jffc_seg_kernel (cooperative launch)");
     } else {
-        jffc_seg_kernel<CMAX, IL4><<<blocks, 32, 0, st>>>(A);
+        jffc_seg_kernel<CMAX, IL4><<<blocks, 32 * SEG_WPB, smem, st>>>(A);
     }
     int rc = check_launch("jffc_seg_kernel");
     if (rc) return rc;
@@ -873,12 +904,12 @@ static int launch(const Plan& pl, Args A, cudaStream_t st) {
         fprintf(stderr, "jffc_seg_kernel %.3f ms\n", ms);
         cudaEventDestroy(ev0);
         cudaEventDestroy(ev1);
-        std::vector<unsigned long long> h((size_t)4 * blocks);
+        std::vector<unsigned long long> h((size_t)4 * units);
         cudaMemcpyAsync(h.data(), A.trace, h.size() * 8, cudaMemcpyDeviceToHost, st);
         cudaStreamSynchronize(st);
         cudaFree(A.trace);
         unsigned long long t0 = ~0ull;
-        for (int b = 0; b < blocks; b++) t0 = std::min(t0, h[4 * b]);
+        for (int b = 0; b < units; b++) t0 = std::min(t0, h[4 * b]);
         for (int s = 0; s < pl.S; s++) {
             std::vector<double> v[4];
             for (int g = 0; g < pl.G; g++)

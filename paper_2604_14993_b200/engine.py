@@ -135,22 +135,21 @@ class SweepEngine:
 
     def run_pipelined(self, steps: int, after_stats=None) -> int:
         """`steps` complete sweeps over two buffer sets and two CUDA streams,
-        in one deterministic order per sweep k: the simulation (alone on the
-        GPU: its cooperative launch keeps one block per resident slot on every
-        SM), then -- beside each other -- the statistics of sweep k and the
-        exponential streams of sweep k+1.  The stream kernel fills whole SMs
-        (16 warps per block, ceil(R/16) blocks) and its stream has the higher
-        priority, so it takes its SMs the moment the simulation ends and the
-        statistics pass runs on the rest.  Every sweep is computed in full;
-        the caller's stream waits for all of them.  ``after_stats(b, stream)``
+        in one deterministic order per sweep k: the simulation (a cooperative
+        launch of whole-SM blocks: ceil(units / 16) SMs, 128 of 148 on config
+        2), beside it on the SMs it leaves free the exponential streams of
+        sweep k+1 (lower priority; they finish beside the statistics), then
+        the statistics of sweep k.  Every sweep is computed in full; the
+        caller's stream waits for all of them.  ``after_stats(b, stream)``
         runs after each sweep's statistics (e.g. the cross-GPU gather of its
         summaries; the statistics' NCCL collectives are in the same stream).
         Returns the last sweep's set."""
         torch = self.torch
         if len(self.sets) < 2:
             self.sets.append(self._alloc_set())
-            # lower number = higher priority (torch clamps to the device's range)
-            self.pipe = [torch.cuda.Stream(priority=-8), torch.cuda.Stream(priority=0)]
+            # lower number = higher priority (torch clamps to the device's range):
+            # the simulation and the statistics chain first, the streams fill in
+            self.pipe = [torch.cuda.Stream(priority=0), torch.cuda.Stream(priority=-8)]
         s_gen, s_sim = self.pipe
         cur = torch.cuda.current_stream()
         for s_ in self.pipe:
@@ -165,8 +164,11 @@ class SweepEngine:
             s_sim.wait_event(ev_gen[b])
             self.simulate(b, s_sim)
             ev_sim[b].record(s_sim)
-            if k + 1 < steps:  # set (k+1)&1 was last read by sweep k-1 (done before sweep k)
-                s_gen.wait_event(ev_sim[b])
+            if k + 1 < steps:
+                # set (k+1)&1 was last simulated by sweep k-1 (its statistics
+                # read only the responses): the streams of sweep k+1 start
+                # beside the simulation of sweep k, on the SMs it leaves free
+                s_gen.wait_event(ev_sim[(k + 1) & 1])
                 self.streams((k + 1) & 1, s_gen, whole_sm=True)
                 ev_gen[(k + 1) & 1].record(s_gen)
             self.statistics(b, s_sim)
