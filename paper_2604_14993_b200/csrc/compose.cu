@@ -222,6 +222,9 @@ __global__ void __launch_bounds__(512) gca_kernel(
     int32_t* dstamp = boff + max_levels + 1;   // [max_levels] round in which a bucket's label changed
     int32_t* chstamp = dstamp + max_levels;    // [max_nodes] round in which a node's label changed
     int32_t* rstamp = chstamp + max_nodes;     // [max_nodes] round whose live predecessor set shrank
+    int32_t* posn = rstamp + max_nodes;        // [max_nodes] node -> its position in `bucket`
+    int32_t* pfr = posn + max_nodes;           // [max_nodes] position -> frontier of its node
+    double* pcost = reinterpret_cast<double*>(((uintptr_t)(pfr + max_nodes) + 7) & ~(uintptr_t)7);  // position -> label cost
     __shared__ int s_nodes, s_status, s_found, s_cap_fail;
     __shared__ unsigned long long s_edges;
     __shared__ int32_t s_path_len;
@@ -313,7 +316,12 @@ __global__ void __launch_bounds__(512) gca_kernel(
             boff[f] = acc;
             acc += c;
         }
-        for (int v = 0; v < V; v++) bucket[boff[nd[v].fr]++] = v;
+        for (int v = 0; v < V; v++) {
+            const int e = boff[nd[v].fr]++;
+            bucket[e] = v;
+            posn[v] = e;
+            pfr[e] = nd[v].fr;
+        }
         for (int f = L + 3; f > 0; f--) boff[f] = boff[f - 1];
         boff[0] = 0;
     }
@@ -331,6 +339,7 @@ __global__ void __launch_bounds__(512) gca_kernel(
         nd[v].depth = 0;
         chstamp[v] = -1;
         rstamp[v] = -1;
+        pcost[posn[v]] = v == 0 ? 0.0 : INFINITY;
     }
     for (int f = tid; f < max_levels; f += nthr) dstamp[f] = -1;
     __syncthreads();
@@ -362,38 +371,48 @@ __global__ void __launch_bounds__(512) gca_kernel(
                     }
                     if (!dirty) continue;  // same live set, same predecessor labels
                 }
+                // scan of the live predecessors by bucket position: their label
+                // costs and frontiers sit in position order (no node lookup);
+                // ties within a lane by path order (Python tuples)
                 double best = INFINITY;
-                int bu = -1;
+                int be = -1;  // best position
                 if (lo <= hi) {
                     for (int e = boff[lo] + lane; e < boff[hi + 1]; e += 32) {
-                        const int u = bucket[e];
-                        const double cu = nd[u].cost;
+                        const double cu = pcost[e];
                         if (!(cu < INFINITY)) continue;
                         const double w =
-                            v == TAIL ? 0.0
-                                      : __dadd_rn(nv.tc, __dmul_rn(nv.tp, (double)(nv.rb + 1 - nd[u].fr)));
+                            v == TAIL ? 0.0 : __dadd_rn(nv.tc, __dmul_rn(nv.tp, (double)(nv.rb + 1 - pfr[e])));
                         const double c = __dadd_rn(cu, w);
-                        if (bu < 0 || c < best || (c == best && lex_less(nd, u, bu, v))) {
+                        if (be < 0 || c < best || (c == best && lex_less(nd, bucket[e], bucket[be], v))) {
                             best = c;
-                            bu = u;
+                            be = e;
                         }
                     }
                 }
-                // warp argmin on (cost, path)
-#pragma unroll
-                for (int d = 16; d > 0; d >>= 1) {
-                    const double ob = __shfl_down_sync(0xffffffffu, best, d);
-                    const int ou = __shfl_down_sync(0xffffffffu, bu, d);
-                    if (ou >= 0 && (bu < 0 || ob < best || (ob == best && lex_less(nd, ou, bu, v)))) {
-                        best = ob;
-                        bu = ou;
+                // warp argmin: costs are >= 0, so their bit patterns order as
+                // the values; two 32-bit min-reductions, exact cost ties across
+                // lanes (rare) by path order
+                const uint64_t cb = be >= 0 ? (uint64_t)__double_as_longlong(best) : ~0ull;
+                const uint32_t chi = (uint32_t)(cb >> 32);
+                const uint32_t mhi = __reduce_min_sync(0xffffffffu, chi);
+                const uint32_t mlo = __reduce_min_sync(0xffffffffu, chi == mhi ? (uint32_t)cb : 0xffffffffu);
+                const unsigned wm = __ballot_sync(0xffffffffu, be >= 0 && chi == mhi && (uint32_t)cb == mlo);
+                int bu = -1;
+                if (wm) {
+                    int bpos = __shfl_sync(0xffffffffu, be, __ffs(wm) - 1);
+                    best = __shfl_sync(0xffffffffu, best, __ffs(wm) - 1);
+                    for (unsigned m = wm & (wm - 1); m; m &= m - 1) {
+                        const int cand = __shfl_sync(0xffffffffu, be, __ffs(m) - 1);
+                        if (lex_less(nd, bucket[cand], bucket[bpos], v)) bpos = cand;
                     }
+                    bu = bucket[bpos];
                 }
                 if (lane == 0) {
                     const int op = nd[v].parent;
                     const bool changed = bu != op || (bu >= 0 && (best != nd[v].cost || chstamp[bu] == its));
                     if (changed) {
                         nd[v].cost = bu >= 0 ? best : INFINITY;
+                        pcost[posn[v]] = bu >= 0 ? best : INFINITY;
                         nd[v].parent = bu;
                         nd[v].depth = bu >= 0 ? nd[bu].depth + 1 : 0;
                         chstamp[v] = its;
@@ -502,7 +521,7 @@ extern "C" int cs_gca_batch_impl(const cs_compose_point* d_points, int32_t n_poi
     const int max_nodes = max_servers + 2;
     const int max_levels = max_blocks_L + 4;
     const size_t smem = sizeof(GcaNode) * max_nodes + sizeof(int32_t) * (max_nodes + max_levels + 1) +
-                        sizeof(int32_t) * (max_levels + 2 * (size_t)max_nodes);
+                        sizeof(int32_t) * (max_levels + 4 * (size_t)max_nodes + 1) + sizeof(double) * max_nodes + 8;
     if (smem > 220 * 1024) {
         set_error("cs_gca_batch: %d servers per point exceeds shared memory", max_servers);
         return CS_UNSUPPORTED;
