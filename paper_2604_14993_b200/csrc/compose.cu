@@ -206,6 +206,10 @@ __device__ bool lex_less(const GcaNode* __restrict__ nd, int u1, int u2, int v) 
 
 // PySum (cs_internal.cuh): CPython >= 3.12 builtin sum() of floats.
 
+#ifndef GCA_SPIN_NS
+#define GCA_SPIN_NS 20  // back-off of a warp waiting for its predecessors' buckets
+#endif
+
 __global__ void __launch_bounds__(512) gca_kernel(
     const cs_compose_point* __restrict__ pts, const int64_t* __restrict__ mem,
     const double* __restrict__ tau_c, const double* __restrict__ tau_p,
@@ -219,9 +223,10 @@ __global__ void __launch_bounds__(512) gca_kernel(
     GcaNode* nd = reinterpret_cast<GcaNode*>(smem);
     int32_t* bucket = reinterpret_cast<int32_t*>(nd + max_nodes);  // nodes sorted by frontier
     int32_t* boff = bucket + max_nodes;                            // bucket offsets [0, L+3]
-    int32_t* dstamp = boff + max_levels + 1;   // [max_levels] round in which a bucket's label changed
-    int32_t* chstamp = dstamp + max_levels;    // [max_nodes] round in which a node's label changed
-    int32_t* rstamp = chstamp + max_nodes;     // [max_nodes] round whose live predecessor set shrank
+    int32_t* bcnt = boff + max_levels + 1;     // [max_levels] labels finished in a bucket, all rounds
+    int32_t* dstamp = bcnt + max_levels;       // [max_levels] round in which a bucket had a label change
+    int32_t* chstamp = dstamp + max_levels;    // [max_nodes] position -> round in which its label changed
+    int32_t* rstamp = chstamp + max_nodes;     // [max_nodes] node -> round whose live predecessor set shrank
     int32_t* posn = rstamp + max_nodes;        // [max_nodes] node -> its position in `bucket`
     int32_t* pfr = posn + max_nodes;           // [max_nodes] position -> frontier of its node
     double* pcost = reinterpret_cast<double*>(((uintptr_t)(pfr + max_nodes) + 7) & ~(uintptr_t)7);  // position -> label cost
@@ -337,56 +342,61 @@ __global__ void __launch_bounds__(512) gca_kernel(
         nd[v].cost = v == 0 ? 0.0 : INFINITY;
         nd[v].parent = -1;
         nd[v].depth = 0;
-        chstamp[v] = -1;
+        chstamp[posn[v]] = -1;
         rstamp[v] = -1;
         pcost[posn[v]] = v == 0 ? 0.0 : INFINITY;
     }
-    for (int f = tid; f < max_levels; f += nthr) dstamp[f] = -1;
+    for (int f = tid; f < max_levels; f += nthr) {
+        bcnt[f] = 0;
+        dstamp[f] = -1;
+    }
     __syncthreads();
     int K = 0;
     int64_t it = 0;
     for (it = 0; it <= E; it++) {
         const int32_t its = (int32_t)it;
-        // --- DP labels in frontier order (round 0: every node; later rounds:
-        //     the nodes whose live set or some predecessor's label changed) ---
-        for (int F = 2; F <= L + 2; F++) {
-            const int nb = boff[F + 1] - boff[F];
-            for (int q = warp; q < nb; q += nwarps) {
-                const int v = bucket[boff[F] + q];
-                const GcaNode& nv = nd[v];
-                int lo = nv.ra;
-                if (v != TAIL) {
-                    const int64_t need = (int64_t)nv.rb + 1 - nv.resid;  // f_u >= need
-                    if (need > lo) lo = need > (int64_t)(L + 3) ? L + 3 : (int)need;
-                }
-                const int hi = nv.rb;
-                if (its > 0 && rstamp[v] != its) {
-                    bool dirty = false;
-                    for (int f0 = lo; f0 <= hi; f0 += 32) {
-                        const int f = f0 + lane;
-                        if (__any_sync(0xffffffffu, f <= hi && dstamp[f] == its)) {
-                            dirty = true;
-                            break;
-                        }
-                    }
-                    if (!dirty) continue;  // same live set, same predecessor labels
-                }
+        // --- DP labels in frontier order, without block barriers: warp w takes
+        //     the nodes at bucket positions boff[2] + w, + nwarps, ... in order
+        //     and waits only for its live predecessors' labels of this round
+        //     (lower positions: the lowest unfinished node can always go on):
+        //     bucket f is final in round `it` once bcnt[f] = (it+1) x its size.
+        //     Round 0 labels every node; later rounds recompute a node only if
+        //     its live set shrank (the last chain's servers) or a predecessor's
+        //     label changed (its bucket stamped), else it keeps its label. ---
+        volatile int32_t* vcnt = bcnt;
+        for (int e0 = boff[2] + warp; e0 < boff[L + 3]; e0 += nwarps) {
+            const int v = bucket[e0];
+            const GcaNode& nv = nd[v];
+            int lo = nv.ra;
+            if (v != TAIL) {
+                const int64_t need = (int64_t)nv.rb + 1 - nv.resid;  // f_u >= need
+                if (need > lo) lo = need > (int64_t)(L + 3) ? L + 3 : (int)need;
+            }
+            const int hi = nv.rb;
+            const int p0 = lo <= hi ? boff[lo] : 0, p1 = lo <= hi ? boff[hi + 1] : 0;
+            bool dirty = its == 0 || rstamp[v] == its;
+            for (int fb = (lo > 2 ? lo : 2); fb <= hi; fb += 32) {  // bucket 1: the head, always final
+                const int f = fb + lane;
+                const int need = f <= hi ? (its + 1) * (boff[f + 1] - boff[f]) : 0;
+                while (!__all_sync(0xffffffffu, f > hi || vcnt[f] >= need)) __nanosleep(GCA_SPIN_NS);
+                __threadfence_block();  // acquire: the predecessors' labels
+                dirty = dirty || __any_sync(0xffffffffu, f <= hi && dstamp[f] == its);
+            }
+            if (dirty) {
                 // scan of the live predecessors by bucket position: their label
                 // costs and frontiers sit in position order (no node lookup);
                 // ties within a lane by path order (Python tuples)
                 double best = INFINITY;
                 int be = -1;  // best position
-                if (lo <= hi) {
-                    for (int e = boff[lo] + lane; e < boff[hi + 1]; e += 32) {
-                        const double cu = pcost[e];
-                        if (!(cu < INFINITY)) continue;
-                        const double w =
-                            v == TAIL ? 0.0 : __dadd_rn(nv.tc, __dmul_rn(nv.tp, (double)(nv.rb + 1 - pfr[e])));
-                        const double c = __dadd_rn(cu, w);
-                        if (be < 0 || c < best || (c == best && lex_less(nd, bucket[e], bucket[be], v))) {
-                            best = c;
-                            be = e;
-                        }
+                for (int e = p0 + lane; e < p1; e += 32) {
+                    const double cu = pcost[e];
+                    if (!(cu < INFINITY)) continue;
+                    const double w =
+                        v == TAIL ? 0.0 : __dadd_rn(nv.tc, __dmul_rn(nv.tp, (double)(nv.rb + 1 - pfr[e])));
+                    const double c = __dadd_rn(cu, w);
+                    if (be < 0 || c < best || (c == best && lex_less(nd, bucket[e], bucket[be], v))) {
+                        best = c;
+                        be = e;
                     }
                 }
                 // warp argmin: costs are >= 0, so their bit patterns order as
@@ -409,19 +419,25 @@ __global__ void __launch_bounds__(512) gca_kernel(
                 }
                 if (lane == 0) {
                     const int op = nd[v].parent;
-                    const bool changed = bu != op || (bu >= 0 && (best != nd[v].cost || chstamp[bu] == its));
+                    const bool changed =
+                        bu != op || (bu >= 0 && (best != nd[v].cost || chstamp[posn[bu]] == its));
                     if (changed) {
                         nd[v].cost = bu >= 0 ? best : INFINITY;
-                        pcost[posn[v]] = bu >= 0 ? best : INFINITY;
+                        pcost[e0] = bu >= 0 ? best : INFINITY;
                         nd[v].parent = bu;
                         nd[v].depth = bu >= 0 ? nd[bu].depth + 1 : 0;
-                        chstamp[v] = its;
+                        chstamp[e0] = its;
                         dstamp[nv.fr] = its;
                     }
                 }
             }
-            __syncthreads();
+            __syncwarp();
+            if (lane == 0) {
+                __threadfence_block();  // release: the label before its count
+                atomicAdd(&bcnt[nv.fr], 1);
+            }
         }
+        __syncthreads();
         if (nd[TAIL].parent < 0) break;  // tail unreachable: allocation done
         // --- allocate the chain (one thread; cache_alloc.py:115-131) ---
         if (tid == 0) {
@@ -521,7 +537,7 @@ extern "C" int cs_gca_batch_impl(const cs_compose_point* d_points, int32_t n_poi
     const int max_nodes = max_servers + 2;
     const int max_levels = max_blocks_L + 4;
     const size_t smem = sizeof(GcaNode) * max_nodes + sizeof(int32_t) * (max_nodes + max_levels + 1) +
-                        sizeof(int32_t) * (max_levels + 4 * (size_t)max_nodes + 1) + sizeof(double) * max_nodes + 8;
+                        sizeof(int32_t) * (2 * (size_t)max_levels + 4 * (size_t)max_nodes) + sizeof(double) * max_nodes + 8;
     if (smem > 220 * 1024) {
         set_error("cs_gca_batch: %d servers per point exceeds shared memory", max_servers);
         return CS_UNSUPPORTED;
