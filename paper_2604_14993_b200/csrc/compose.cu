@@ -50,8 +50,10 @@ __global__ void __launch_bounds__(1024) gbp_kernel(
     const int32_t* __restrict__ id_rank, int32_t* __restrict__ first, int32_t* __restrict__ count,
     int32_t* __restrict__ max_blocks, double* __restrict__ bound_time, int32_t* __restrict__ order,
     int32_t* __restrict__ chain_end, int32_t* __restrict__ n_chains, double* __restrict__ scaled_rate,
-    int32_t* __restrict__ rate_satisfied, int32_t* __restrict__ status, int32_t sort_cap) {
-    extern __shared__ SortKey keys[];  // sort_cap entries (power of two)
+    int32_t* __restrict__ rate_satisfied, int32_t* __restrict__ status, int32_t sort_cap, int32_t mt_smem) {
+    extern __shared__ SortKey keys[];  // sort_cap entries (power of two), then per server m_j, t_j
+    int32_t* s_m = reinterpret_cast<int32_t*>(keys + sort_cap);
+    double* s_t = reinterpret_cast<double*>(keys + sort_cap) + (sort_cap + 1) / 2;
     __shared__ int n_keys;
     const cs_compose_point pt = pts[blockIdx.x];
     const int J = pt.n_servers;
@@ -75,6 +77,10 @@ __global__ void __launch_bounds__(1024) gbp_kernel(
         const double t = __dadd_rn(tau_c[sb + j], __dmul_rn(tau_p[sb + j], (double)m));
         max_blocks[sb + j] = (int32_t)m;
         bound_time[sb + j] = t;
+        if (mt_smem) {  // the greedy scan below reads them from shared memory
+            s_m[j] = (int32_t)m;
+            s_t[j] = t;
+        }
         first[sb + j] = 0;
         count[sb + j] = 0;
         order[sb + j] = -1;
@@ -128,12 +134,12 @@ __global__ void __launch_bounds__(1024) gbp_kernel(
     int nch = 0, cur_begin = 0, q = 0;
     for (; q < nk; q++) {
         const int j = keys[q].idx;
-        const int64_t m = max_blocks[sb + j];
+        const int64_t m = mt_smem ? s_m[j] : max_blocks[sb + j];
         const int64_t a = frontier < L - m + 1 ? frontier : L - m + 1;
         first[sb + j] = (int32_t)a;
         count[sb + j] = (int32_t)m;
         order[sb + q] = j;
-        chain_time = __dadd_rn(chain_time, bound_time[sb + j]);
+        chain_time = __dadd_rn(chain_time, mt_smem ? s_t[j] : bound_time[sb + j]);
         const int64_t fr = frontier + m - 1;
         frontier = (fr < L ? fr : L) + 1;
         if (frontier > L) {
@@ -150,7 +156,7 @@ __global__ void __launch_bounds__(1024) gbp_kernel(
         }
     }
     for (int u = cur_begin; u < q; u++) {  // incomplete trailing chain is cleared
-        const int j = order[sb + u];
+        const int j = keys[u].idx;
         first[sb + j] = 0;
         count[sb + j] = 0;
         order[sb + u] = -1;
@@ -510,7 +516,9 @@ extern "C" int cs_gbp_batch_impl(const cs_compose_point* d_points, int32_t n_poi
     int cap = 1;
     while (cap < max_servers) cap <<= 1;
     if (cap < 32) cap = 32;
-    const size_t smem = sizeof(SortKey) * cap;
+    size_t smem = sizeof(SortKey) * cap + sizeof(double) * ((cap + 1) / 2 + cap);
+    const int mt_smem = smem <= 200 * 1024;  // else the scan reads m_j, t_j from global memory
+    if (!mt_smem) smem = sizeof(SortKey) * cap;
     if (smem > 200 * 1024) {
         set_error("cs_gbp_batch: %d servers per point exceeds the shared-memory sort (max 12800)",
                   max_servers);
@@ -520,7 +528,7 @@ extern "C" int cs_gbp_batch_impl(const cs_compose_point* d_points, int32_t n_poi
     const int threads = cap >= 1024 ? 1024 : cap;
     gbp_kernel<<<n_points, threads, smem, (cudaStream_t)stream>>>(
         d_points, d_mem, d_tau_c, d_tau_p, d_id_rank, d_first, d_count, d_max_blocks, d_bound_time,
-        d_order, d_chain_end, d_n_chains, d_scaled_rate, d_rate_satisfied, d_status, cap);
+        d_order, d_chain_end, d_n_chains, d_scaled_rate, d_rate_satisfied, d_status, cap, mt_smem);
     return check_launch("gbp_kernel");
 }
 
