@@ -476,6 +476,15 @@ def main():
         roof["traffic"] = sum(k[x]["dram_read"] + k[x]["dram_write"] for x in sim_k)
         roof["ncu"] = {"source": os.path.relpath(NCU_SUMMARY, ROOT), "inst_executed_per_sweep": sim_inst,
                        "kernels": {x: k[x] for x in sim_k}}
+        row_k = [x for x in k if x.split("<")[0].endswith("row_stats_kernel")]
+        if row_k:  # the row pass alone (ncu launch list of the same build: device time per launch)
+            rk = k[row_k[0]]
+            roof["stats_pass"]["row_kernel"] = {
+                "kernel": rk.get("kernel", row_k[0]), "duration_ms": rk["duration_ms"],
+                "achieved": stats_bytes / (rk["duration_ms"] / 1e3) / 1e9,
+                "frac": stats_bytes / (rk["duration_ms"] / 1e3) / 1e9 / peak,
+                "traffic": rk["dram_read"] + rk["dram_write"], "issue_active_pct": rk.get("issue_active_pct"),
+                "source": os.path.relpath(NCU_SUMMARY, ROOT)}
 
     # end to end through the public API (host buffers in/out), rank-local work
     cfgs = [P.SimConfig(rates=rates, capacities=caps, workload=P.PoissonWorkload(l),

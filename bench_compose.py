@@ -86,7 +86,14 @@ def run(regime: str, n_inst: int, steps: int, cpu_sample: int):
             prof = json.load(fh).get(regime)
     roof = {"bound": "issue", "relaxations_per_instance": relax / n_inst,
             "relaxations_per_s": relax / (gca_ms / 1e3), "unit": "edge relaxations/s (K x E bound)",
+            "note": "K x E = the relaxations the reference's per-round Dijkstra performs; the GPU's rounds "
+                    "after the first rescan only nodes whose live set or predecessor labels changed, so this "
+                    "is the reference-equivalent work rate; the kernel's own bound is issue/latency "
+                    "(ncu issue-slot utilisation below)",
             "ncu": prof}
+    if prof and "gca_kernel" in prof and "Issue Slots Busy" in prof["gca_kernel"]:
+        roof["frac"] = float(prof["gca_kernel"]["Issue Slots Busy"].split()[-1]) / 100.0
+        roof["frac_of"] = "gca_kernel issue slots busy (ncu, profiles/r2_ncu_compose.json)"
     return {
         "metric": "composed instances/sec (GBP-CR + GCA)", "regime": regime,
         "value": n_inst / (total_ms / 1e3), "unit": "instances/s", "n_gpus": 1, "steps": steps,

@@ -89,31 +89,34 @@ METRICS = ("Duration", "DRAM Throughput", "Memory Throughput", "L1/TEX Hit Rate"
 
 def full(src):
     out = ["# r2: ncu --set full --clock-control none (profiles/profile_r2.sh): simulator, row statistics,",
-           "# stream kernel (config 2 bench sweep) and GBP/GCA (config 4, 256 full-fleet instances)"]
+           "# stream kernel (config 2 bench sweep) and GBP/GCA (config 4, 2000 instances per regime)"]
     comp = {}
-    for name in ("prof_seg", "prof_stats", "prof_streams", "prof_compose"):
+    for name in ("prof_seg", "prof_stats", "prof_streams", "prof_compose_moderate", "prof_compose_full"):
         rep = os.path.join(src, name + ".ncu-rep")
         if not os.path.exists(rep):
             continue
+        regime = name.split("_")[-1] if name.startswith("prof_compose") else None
         txt = subprocess.run(["ncu", "-i", rep, "--page", "details"], capture_output=True, text=True).stdout
         kernel = None
         for line in txt.splitlines():
             if "Context" in line and "Stream" in line and "(" in line:
                 kernel = short(line.strip())
-                out.append(f"\n== {kernel}")
+                out.append(f"\n== {kernel}" + (f"  [config 4, {regime}]" if regime else ""))
             s = line.strip()
             for m in METRICS:
                 if s.startswith(m + " ") or s.startswith(m + "  "):
                     out.append("  " + " ".join(s.split()))
-                    if name == "prof_compose" and kernel and m in ("Issue Slots Busy", "Duration",
-                                                                    "Executed Instructions", "Achieved Occupancy"):
-                        comp.setdefault(kernel.split("<")[0], {})[m] = " ".join(s.split()[len(m.split()):])
+                    if regime and kernel and m in ("Issue Slots Busy", "Duration",
+                                                   "Executed Instructions", "Achieved Occupancy"):
+                        comp.setdefault(regime, {}).setdefault(kernel.split("<")[0], {})[m] = \
+                            " ".join(s.split()[len(m.split()):])
     with open(os.path.join(HERE, "r2_ncu_full_summary.txt"), "w") as fh:
         fh.write("\n".join(out) + "\n")
     if comp:
+        comp["source"] = ("profiles/profile_r2.sh: ncu --set full, bench_compose.py --regime "
+                          "{moderate,full} --instances 2000")
         with open(os.path.join(HERE, "r2_ncu_compose.json"), "w") as fh:
-            json.dump({"full": comp, "source": "profiles/profile_r2.sh: ncu --set full, bench_compose.py "
-                                               "--regime full --instances 256"}, fh, indent=1)
+            json.dump(comp, fh, indent=1)
     print("\n".join(out))
 
 

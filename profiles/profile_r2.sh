@@ -5,7 +5,7 @@
 #   prof_seg.ncu-rep    ncu --set full of the segmented simulator
 #   prof_stats.ncu-rep  ncu --set full of the row-statistics pass
 #   prof_streams.ncu-rep ncu --set full of the stream (+ prefix) kernel
-#   prof_compose.ncu-rep ncu --set full of gbp_kernel and gca_kernel (full-fleet config 4)
+#   prof_compose_{moderate,full}.ncu-rep ncu --set full of gbp_kernel and gca_kernel (config 4, 2000 instances)
 # Each ncu command follows the same command line run plain (exit 0) first.
 set -x
 mkdir -p gpurun_out
@@ -19,8 +19,10 @@ ncu --set full --import-source on --clock-control none -k regex:row_stats -c 1 \
     -o gpurun_out/prof_stats $B > gpurun_out/prof_stats.log 2>&1
 ncu --set full --import-source on --clock-control none -k regex:exp_streams -c 1 \
     -o gpurun_out/prof_streams $B > gpurun_out/prof_streams.log 2>&1
-C="python bench_compose.py --regime full --instances 256 --steps 1 --cpu-sample 1"
-$C > gpurun_out/prof_compose_plain.log 2>&1 || exit 1
-ncu --set full --import-source on --clock-control none -k regex:"gbp_kernel|gca_kernel" -c 2 \
-    -o gpurun_out/prof_compose $C > gpurun_out/prof_compose.log 2>&1
+for R in moderate full; do
+  C="python bench_compose.py --regime $R --instances 2000 --steps 1 --cpu-sample 1"
+  $C > gpurun_out/prof_compose_${R}_plain.log 2>&1 || exit 1
+  ncu --set full --import-source on --clock-control none -k regex:"gbp_kernel|gca_kernel" -c 2 \
+      -o gpurun_out/prof_compose_$R $C > gpurun_out/prof_compose_$R.log 2>&1
+done
 echo done
