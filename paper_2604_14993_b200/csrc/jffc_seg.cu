@@ -116,6 +116,7 @@ struct Args {
     uint32_t* ckk;     // [S][G][Q][CMAX][32]       keys
     double* blk;       // [NB][NAGG][T]             per-block sums
     int32_t* status;   // [S][T]
+    int32_t* spec;     // [S][T] 1 once the row's speculative phase 2 has stopped (writes visible)
     uint32_t* progress;  // [S][G]
     int32_t nseg, G, Q, cmax;
     int64_t nblk;
@@ -642,16 +643,53 @@ __global__ void __launch_bounds__(32 * SEG_WPB, 1) jffc_seg_kernel(Args A) {
     __syncwarp();
     if (lane == 0) st_release(A.progress + unit, DONE | (uint32_t)Q);
 
-    // ---- phase 2: continue only where this segment is known to be exact
-    if (s > 0) {
-        int32_t stv = valid ? ST_UNKNOWN : ST_SKIPPED;
-        while (__any_sync(FULL, stv == ST_UNKNOWN)) {
-            if (stv == ST_UNKNOWN) stv = ld_relaxed(A.status + (int64_t)s * T + tid);
-            if (__any_sync(FULL, stv == ST_UNKNOWN)) __nanosleep(256);
+    // ---- phase 2, speculative: every lane runs on past its range at once,
+    // as if this segment were exact, and polls its verdict every chunk (set
+    // by the exact run that couples into this segment -- exact -- or that
+    // passes through it -- SKIPPED).  If the verdict is exact, the run from
+    // here on is exact too (this segment's trajectory has been the true one
+    // since the coupling point).  If SKIPPED, the lane stops; everything it
+    // wrote past its range is rewritten by the exact run, which enters the
+    // next range only after this lane's spec flag (all its writes visible).
+    // The decisions this lane takes about later segments (passed through:
+    // SKIPPED; coupled into: exact) are released only once its own verdict is
+    // exact.  Waits only run forward (frontier gating, spec flags of later
+    // segments; the last segment has no phase 2): no deadlock.  Round 1's
+    // form waited for the verdict first, which serialised the hand-overs of
+    // a row into a chain (the kernel's last 1.5 ms on config 2).
+    int32_t stv = !valid ? ST_SKIPPED : s == 0 ? 2 : ST_UNKNOWN;
+    act = valid;
+    int32_t skip_to = s + 1;           // segments [s + 1, skip_to) passed through (unreleased)
+    int32_t hand_t = -1, hand_j = 0;   // coupled into hand_t at job hand_j (unreleased)
+    bool flagged = false;              // spec flag set
+    int32_t* const spec_s = A.spec + (int64_t)s * T + tid;
+    auto release_pending = [&]() {     // this lane's verdict is exact
+        for (int32_t u = s + 1; u < skip_to; u++) st_release(A.status + (int64_t)u * T + tid, ST_SKIPPED);
+        skip_to = s + 1;
+        if (hand_t >= 0) st_release(A.status + (int64_t)hand_t * T + tid, (int32_t)(2 + hand_j));
+        hand_t = -1;
+    };
+    auto stop_lanes = [&](bool who) {  // warp-uniform call: the lanes in `who` stop
+        __threadfence();
+        if (who && valid && !flagged) {
+            st_release(spec_s, 1);
+            flagged = true;
         }
-        fence_acquire();
-        act = valid && stv >= 2;
-    }
+    };
+    auto poll = [&]() {  // warp-uniform call
+        bool now_skipped = false;
+        if (act && stv == ST_UNKNOWN) {
+            stv = ld_relaxed(A.status + (int64_t)s * T + tid);
+            if (stv >= 2) {
+                fence_acquire();
+                release_pending();
+            } else if (stv == ST_SKIPPED) {
+                act = false;
+                now_skipped = true;
+            }
+        }
+        if (__any_sync(FULL, now_skipped)) stop_lanes(now_skipped);
+    };
     if (tr && lane == 0) tr[2] = gtimer();
     int t = s + 1;
     while (__any_sync(FULL, act)) {
@@ -720,25 +758,58 @@ __global__ void __launch_bounds__(32 * SEG_WPB, 1) jffc_seg_kernel(Args A) {
                     wait_for([&] { return !same || n_resp <= ft; });
                     flush(true, same);  // our emissions before the hand-over
                     if (same) {
-                        st_release(A.status + (int64_t)t * T + tid, (int32_t)(2 + j));
+                        if (stv >= 2) {
+                            release_pending();
+                            st_release(A.status + (int64_t)t * T + tid, (int32_t)(2 + j));
+                        } else {
+                            hand_t = t;
+                            hand_j = (int32_t)j;
+                        }
                         act = false;
                     }
+                    stop_lanes(same);
                 }
                 q++;
                 next_ck = q <= Q ? bt + ck_offset(q) : INT64_MAX;
             }
+            poll();
         }
         if (j == et && __any_sync(FULL, act)) {
             wait_for([&] { return jt == INT64_MAX; });  // t's range entirely ours from here
             if (et == n) {  // ran through the last segment: these lanes finish the row
                 drain(act);
                 flush(true, act);
+                const bool fin_now = act;
                 act = false;
+                stop_lanes(fin_now);
             } else {
-                if (act) st_release(A.status + (int64_t)t * T + tid, ST_SKIPPED);
+                if (act) {
+                    skip_to = t + 1;
+                    if (stv >= 2) release_pending();
+                }
+                // t's own speculative writes past its range land before ours
+                const int32_t* spec_t = A.spec + (int64_t)t * T + tid;
+                while (!__all_sync(FULL, !act || ld_relaxed(spec_t) != 0)) {
+                    __nanosleep(256);
+                    poll();
+                }
+                fence_acquire();
                 t++;
             }
         }
+    }
+    // this lane has stopped: flag it, then settle its decisions once its own
+    // verdict is known (they only matter if it is exact)
+    stop_lanes(true);
+    while (__any_sync(FULL, valid && stv == ST_UNKNOWN && (hand_t >= 0 || skip_to > s + 1))) {
+        if (valid && stv == ST_UNKNOWN) {
+            stv = ld_relaxed(A.status + (int64_t)s * T + tid);
+            if (stv >= 2) {
+                fence_acquire();
+                release_pending();
+            }
+        }
+        __nanosleep(256);
     }
     if (tr && lane == 0) tr[3] = gtimer();
 }
@@ -798,7 +869,7 @@ __global__ void seg_finalize_kernel(Args A) {
 struct Plan {
     int S, G, Q, cmax;
     int64_t T, nblk;
-    size_t off_prefix, off_ckf, off_ckk, off_blk, off_status, off_progress, bytes;
+    size_t off_prefix, off_ckf, off_ckk, off_blk, off_status, off_spec, off_progress, bytes;
 };
 
 static int pick_cmax(int32_t max_cap) { return max_cap <= 4 ? 4 : max_cap <= 7 ? 7 : max_cap <= 8 ? 8 : 16; }
@@ -864,6 +935,8 @@ static Plan make_plan(int32_t P, int32_t R, int32_t max_cap, int64_t n) {
     pl.off_blk = off;
     off = align256(off + sizeof(double) * (size_t)pl.nblk * NAGG * pl.T);
     pl.off_status = off;
+    off = align256(off + sizeof(int32_t) * (size_t)S * pl.T);
+    pl.off_spec = off;
     off = align256(off + sizeof(int32_t) * (size_t)S * pl.T);
     pl.off_progress = off;
     off = align256(off + sizeof(uint32_t) * (size_t)S * pl.G);
@@ -1021,6 +1094,7 @@ extern "C" int cs_seg_sim_impl(const cs_sim_point* d_points, int32_t P, const do
     A.ckk = (uint32_t*)(ws + pl.off_ckk);
     A.blk = (double*)(ws + pl.off_blk);
     A.status = (int32_t*)(ws + pl.off_status);
+    A.spec = (int32_t*)(ws + pl.off_spec);
     A.progress = (uint32_t*)(ws + pl.off_progress);
     A.nblk = pl.nblk;
     A.nseg = pl.S;
