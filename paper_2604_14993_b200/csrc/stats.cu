@@ -522,6 +522,146 @@ __global__ void __launch_bounds__(LB_WARPS * 32, 2) row_stats_kernel(
     }
 }
 
+// ---------------------------------------------------------------------------
+// Sample brackets on the device (the sample only has to bracket each target;
+// the full pass verifies): per group, the digit-0 histogram of the sample
+// (hist0_rows_kernel) locates each sample rank's 15-bit bucket; a second
+// histogram of the next 15 bits (bits 47..33) over the sample values in those
+// buckets locates it to within 2^33 of its bit pattern -- finer than the
+// whole high-word ranges the brackets are widened to.  No compaction, no
+// digit rounds, one small read-back.
+constexpr int H1_BITS = 15, H1_BINS = 1 << H1_BITS;
+constexpr int SB_SLOTS = 2 * MAX_LISTS;  // sample ranks per group (both bracket ends)
+
+// The bucket of each sample rank (block per group: block scan of the 32K bins
+// in shared memory, then a binary search per rank).  rep[i]: the first slot
+// with the same bucket (its hist1 plane is shared).
+__global__ void __launch_bounds__(1024) sb_select0_kernel(const uint32_t* __restrict__ hist0, int n_slots,
+                                                          const int64_t* __restrict__ srank,
+                                                          uint32_t* __restrict__ bucket, int64_t* __restrict__ resid,
+                                                          int32_t* __restrict__ rep) {
+    extern __shared__ uint32_t cum[];  // [H0_BINS] inclusive prefix
+    __shared__ uint32_t part[1024];
+    const uint32_t* h = hist0 + (size_t)blockIdx.x * H0_BINS;
+    constexpr int PER = H0_BINS / 1024;
+    uint32_t loc[PER], acc = 0;
+#pragma unroll
+    for (int k = 0; k < PER; k++) acc += (loc[k] = h[threadIdx.x * PER + k]);
+    part[threadIdx.x] = acc;
+    __syncthreads();
+    for (int d = 1; d < 1024; d <<= 1) {  // inclusive scan of the partial sums
+        const uint32_t v = threadIdx.x >= (unsigned)d ? part[threadIdx.x - d] : 0u;
+        __syncthreads();
+        part[threadIdx.x] += v;
+        __syncthreads();
+    }
+    uint32_t run = threadIdx.x ? part[threadIdx.x - 1] : 0u;
+#pragma unroll
+    for (int k = 0; k < PER; k++) cum[threadIdx.x * PER + k] = (run += loc[k]);
+    __syncthreads();
+    if (threadIdx.x < (unsigned)n_slots) {
+        const int i = threadIdx.x;
+        const int64_t r = srank[(size_t)blockIdx.x * n_slots + i];
+        int lo = 0, hi = H0_BINS - 1;  // first bin with cum > r
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if ((int64_t)cum[mid] > r) hi = mid;
+            else lo = mid + 1;
+        }
+        bucket[(size_t)blockIdx.x * SB_SLOTS + i] = (uint32_t)lo;
+        resid[(size_t)blockIdx.x * SB_SLOTS + i] = r - (lo ? (int64_t)cum[lo - 1] : 0);
+    }
+    __syncthreads();
+    if (threadIdx.x < (unsigned)n_slots) {
+        const int i = threadIdx.x;
+        const uint32_t b = bucket[(size_t)blockIdx.x * SB_SLOTS + i];
+        int r0 = i;
+        for (int j = 0; j < i; j++)
+            if (bucket[(size_t)blockIdx.x * SB_SLOTS + j] == b) {
+                r0 = j;
+                break;
+            }
+        rep[(size_t)blockIdx.x * SB_SLOTS + i] = r0;
+    }
+}
+
+// bits 47..33 of the sample values whose digit 0 is a selected bucket, into
+// the plane of that bucket's first slot (global atomics: the values spread)
+__global__ void __launch_bounds__(256) sb_hist1_kernel(const double* __restrict__ resp, int64_t n_rows, RowView rv,
+                                                       int64_t ldr, int64_t rows_per_group, int n_slots,
+                                                       const uint32_t* __restrict__ bucket,
+                                                       const int32_t* __restrict__ rep,
+                                                       uint32_t* __restrict__ hist1) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); row < n_rows; row += warps) {
+        const int64_t g = row / rows_per_group;
+        uint32_t bk[SB_SLOTS];
+#pragma unroll
+        for (int q = 0; q < SB_SLOTS; q++)
+            bk[q] = q < n_slots && rep[g * SB_SLOTS + q] == q ? bucket[g * SB_SLOTS + q] : 0xffffffffu;
+        const double* __restrict__ a = resp + row * ldr;
+        uint32_t* hg = hist1 + (size_t)g * SB_SLOTS * H1_BINS;
+        constexpr int U = 8;
+        for (int64_t base = 0; base < rv.len; base += 32 * U) {
+            uint64_t u[U];
+#pragma unroll
+            for (int k = 0; k < U; k++) {
+                const int64_t s = base + 32 * k + lane;
+                u[k] = s < rv.len ? dbits(__ldg(a + rv.phys(s))) : ~0ull;
+            }
+#pragma unroll
+            for (int k = 0; k < U; k++) {
+                const uint32_t d0 = (uint32_t)(u[k] >> 48);
+                int ql = -1;
+#pragma unroll
+                for (int q = 0; q < SB_SLOTS; q++)
+                    if (bk[q] == d0) ql = q;
+                if (ql >= 0) atomicAdd(&hg[(size_t)ql * H1_BINS + ((u[k] >> 33) & (H1_BINS - 1))], 1u);
+            }
+        }
+    }
+}
+
+// per (group, slot): the bit prefix (62..33) of the sample order statistic
+__global__ void __launch_bounds__(1024) sb_select1_kernel(const uint32_t* __restrict__ hist1, int n_slots,
+                                                          const uint32_t* __restrict__ bucket,
+                                                          const int64_t* __restrict__ resid,
+                                                          const int32_t* __restrict__ rep,
+                                                          uint64_t* __restrict__ prefix) {
+    extern __shared__ uint32_t cum[];  // [H1_BINS]
+    __shared__ uint32_t part[1024];
+    const int g = blockIdx.x / n_slots, i = blockIdx.x % n_slots;
+    const size_t gi = (size_t)g * SB_SLOTS + i;
+    const uint32_t* h = hist1 + ((size_t)g * SB_SLOTS + rep[gi]) * H1_BINS;
+    constexpr int PER = H1_BINS / 1024;
+    uint32_t loc[PER], acc = 0;
+#pragma unroll
+    for (int k = 0; k < PER; k++) acc += (loc[k] = h[threadIdx.x * PER + k]);
+    part[threadIdx.x] = acc;
+    __syncthreads();
+    for (int d = 1; d < 1024; d <<= 1) {
+        const uint32_t v = threadIdx.x >= (unsigned)d ? part[threadIdx.x - d] : 0u;
+        __syncthreads();
+        part[threadIdx.x] += v;
+        __syncthreads();
+    }
+    uint32_t run = threadIdx.x ? part[threadIdx.x - 1] : 0u;
+#pragma unroll
+    for (int k = 0; k < PER; k++) cum[threadIdx.x * PER + k] = (run += loc[k]);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const int64_t r = resid[gi];
+        int lo = 0, hi = H1_BINS - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if ((int64_t)cum[mid] > r) hi = mid;
+            else lo = mid + 1;
+        }
+        prefix[gi] = ((uint64_t)bucket[gi] << 48) | ((uint64_t)lo << 33);
+    }
+}
+
 struct SelSlot {
     uint64_t prefix;   // fixed high bits (above the current digit)
     int64_t rank;      // remaining rank among the candidates sharing the prefix
@@ -770,6 +910,66 @@ static int select_rows(const double* d_resp, int64_t n_groups, int64_t rows_per_
     return CS_OK;
 }
 
+// Bit prefixes (62..33) of the sample order statistics at srank[g][i]
+// (i < n_slots <= SB_SLOTS) over the logical view rv of every row.
+static int sample_brackets(const double* d_resp, int64_t n_groups, int64_t rows_per_group, RowView rv,
+                           int64_t ldr, const std::vector<int64_t>& srank, int n_slots,
+                           std::vector<uint64_t>& out, bool dist, cudaStream_t st) {
+    const int64_t n_rows = n_groups * rows_per_group;
+    const size_t gs = (size_t)n_groups * SB_SLOTS;
+    int rc;
+    DBuf b_h0, b_bad, b_rank, b_bucket, b_resid, b_rep, b_h1, b_pref;
+    if ((rc = b_h0.alloc(sizeof(uint32_t) * H0_BINS * (size_t)n_groups, st)) ||
+        (rc = b_bad.alloc(sizeof(unsigned long long), st)) ||
+        (rc = b_rank.alloc(sizeof(int64_t) * srank.size(), st)) ||
+        (rc = b_bucket.alloc(sizeof(uint32_t) * gs, st)) || (rc = b_resid.alloc(sizeof(int64_t) * gs, st)) ||
+        (rc = b_rep.alloc(sizeof(int32_t) * gs, st)) ||
+        (rc = b_h1.alloc(sizeof(uint32_t) * H1_BINS * gs, st)) || (rc = b_pref.alloc(sizeof(uint64_t) * gs, st)))
+        return rc;
+    cudaMemsetAsync(b_h0.p, 0, b_h0.n, st);
+    cudaMemsetAsync(b_bad.p, 0, b_bad.n, st);
+    cudaMemsetAsync(b_h1.p, 0, b_h1.n, st);
+    cudaMemcpyAsync(b_rank.p, srank.data(), b_rank.n, cudaMemcpyHostToDevice, st);
+    cudaFuncSetAttribute(hist0_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(sizeof(uint32_t) * H0_BINS));
+    hist0_rows_kernel<<<(int)std::min<int64_t>(n_rows, 2 * sm_count()), 1024, sizeof(uint32_t) * H0_BINS, st>>>(
+        d_resp, n_rows, rv, ldr, rows_per_group, b_h0.as<uint32_t>(), b_bad.as<unsigned long long>());
+    if ((rc = check_launch("hist0_rows_kernel"))) return rc;
+    if (dist && ((rc = allreduce_u32(b_h0.p, (size_t)H0_BINS * n_groups, st)) ||
+                 (rc = allreduce_u64(b_bad.p, 1, st))))
+        return rc;
+    cudaFuncSetAttribute(sb_select0_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(sizeof(uint32_t) * H0_BINS));
+    sb_select0_kernel<<<(unsigned)n_groups, 1024, sizeof(uint32_t) * H0_BINS, st>>>(
+        b_h0.as<uint32_t>(), n_slots, b_rank.as<int64_t>(), b_bucket.as<uint32_t>(), b_resid.as<int64_t>(),
+        b_rep.as<int32_t>());
+    if ((rc = check_launch("sb_select0_kernel"))) return rc;
+    sb_hist1_kernel<<<(unsigned)std::min<int64_t>((n_rows + 7) / 8, (int64_t)sm_count() * 16), 256, 0, st>>>(
+        d_resp, n_rows, rv, ldr, rows_per_group, n_slots, b_bucket.as<uint32_t>(), b_rep.as<int32_t>(),
+        b_h1.as<uint32_t>());
+    if ((rc = check_launch("sb_hist1_kernel"))) return rc;
+    if (dist && (rc = allreduce_u32(b_h1.p, (size_t)H1_BINS * gs, st))) return rc;
+    cudaFuncSetAttribute(sb_select1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(sizeof(uint32_t) * H1_BINS));
+    sb_select1_kernel<<<(unsigned)(n_groups * n_slots), 1024, sizeof(uint32_t) * H1_BINS, st>>>(
+        b_h1.as<uint32_t>(), n_slots, b_bucket.as<uint32_t>(), b_resid.as<int64_t>(), b_rep.as<int32_t>(),
+        b_pref.as<uint64_t>());
+    if ((rc = check_launch("sb_select1_kernel"))) return rc;
+    std::vector<uint64_t> pref(gs);
+    unsigned long long bad = 0;
+    cudaMemcpyAsync(pref.data(), b_pref.p, b_pref.n, cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(&bad, b_bad.p, sizeof(bad), cudaMemcpyDeviceToHost, st);
+    if ((rc = check_cuda(cudaStreamSynchronize(st), "sample brackets sync"))) return rc;
+    if (bad) {
+        set_error("cs_rep_stats: %llu negative responses (impossible for valid input)", bad);
+        return CS_INTERNAL;
+    }
+    out.assign((size_t)n_groups * n_slots, 0);
+    for (int64_t g = 0; g < n_groups; g++)
+        for (int i = 0; i < n_slots; i++) out[g * n_slots + i] = pref[g * SB_SLOTS + i];
+    return CS_OK;
+}
+
 // Split tree of numpy's pairwise sum for rows of m values (cached per m):
 // leaves in order, and the internal nodes grouped by height (leaves 0): a
 // node stores its value in its leftmost leaf's slot, so combining it is
@@ -936,15 +1136,16 @@ extern "C" int cs_rep_stats_impl(const double* d_resp, int32_t n_groups, int64_t
                 r_both[(g * 2 * n_ranks) + q] = r_lo[g * n_ranks + q];
                 r_both[(g * 2 * n_ranks) + n_ranks + q] = r_hi[g * n_ranks + q];
             }
-        std::vector<double> v_both, v_lo(T), v_hi(T);
+        std::vector<uint64_t> p_both, p_lo(T), p_hi(T);  // bit prefixes 62..33 of the sample statistics
         trace("begin", st);
-        if ((rc = select_rows(d_resp, n_groups, rows_per_group, sample, ldr, r_both, 2 * n_ranks, v_both, dist, st)))
+        if ((rc = sample_brackets(d_resp, n_groups, rows_per_group, sample, ldr, r_both, 2 * n_ranks, p_both, dist,
+                                  st)))
             return rc;
-        trace("sample select", st);
+        trace("sample brackets", st);
         for (int64_t g = 0; g < n_groups; g++)
             for (int q = 0; q < n_ranks; q++) {
-                v_lo[g * n_ranks + q] = v_both[g * 2 * n_ranks + q];
-                v_hi[g * n_ranks + q] = v_both[g * 2 * n_ranks + n_ranks + q];
+                p_lo[g * n_ranks + q] = p_both[g * 2 * n_ranks + q];
+                p_hi[g * n_ranks + q] = p_both[g * 2 * n_ranks + n_ranks + q];
             }
         std::vector<int32_t> nlist(n_groups, 0);
         const size_t L6 = (size_t)n_groups * MAX_LISTS;
@@ -954,13 +1155,11 @@ extern "C" int cs_rep_stats_impl(const double* d_resp, int32_t n_groups, int64_t
         for (int64_t g = 0; g < n_groups; g++) {
             std::vector<int> idx(n_ranks);
             for (int q = 0; q < n_ranks; q++) idx[q] = q;
-            // whole high-word ranges: the row pass classifies on the high 32 bits alone
-            auto a_of = [&](int q) {
-                return r_lo[g * n_ranks + q] == 0 ? 0ull : bits_of(v_lo[g * n_ranks + q]) & ~0xffffffffull;
-            };
+            // whole high-word ranges: the row pass classifies on the high 32 bits
+            // alone (a sample statistic lies in [prefix, prefix + 2^33))
+            auto a_of = [&](int q) { return r_lo[g * n_ranks + q] == 0 ? 0ull : p_lo[g * n_ranks + q] & ~0xffffffffull; };
             auto b_of = [&](int q) {
-                return r_hi[g * n_ranks + q] == NS - 1 ? 0x7fffffffffffffffull
-                                                       : bits_of(v_hi[g * n_ranks + q]) | 0xffffffffull;
+                return r_hi[g * n_ranks + q] == NS - 1 ? 0x7fffffffffffffffull : p_hi[g * n_ranks + q] | 0x1ffffffffull;
             };
             std::sort(idx.begin(), idx.end(), [&](int x, int y) { return a_of(x) < a_of(y); });
             for (int q : idx) {
