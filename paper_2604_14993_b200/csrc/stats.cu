@@ -526,11 +526,12 @@ __global__ void __launch_bounds__(LB_WARPS * 32, 2) row_stats_kernel(
 // Sample brackets on the device (the sample only has to bracket each target;
 // the full pass verifies): per group, the digit-0 histogram of the sample
 // (hist0_rows_kernel) locates each sample rank's 15-bit bucket; a second
-// histogram of the next 15 bits (bits 47..33) over the sample values in those
-// buckets locates it to within 2^33 of its bit pattern -- finer than the
-// whole high-word ranges the brackets are widened to.  No compaction, no
+// histogram of the next 12 bits (bits 47..36) over the sample values in those
+// buckets locates it to within 2^36 of its bit pattern (16 high-word units:
+// a relative 2^-16 of its bucket, far inside the +-12 sigma margin).  3 MB of
+// counters for 16 groups: cheap to all-reduce when sharded.  No compaction, no
 // digit rounds, one small read-back.
-constexpr int H1_BITS = 15, H1_BINS = 1 << H1_BITS;
+constexpr int H1_BITS = 12, H1_BINS = 1 << H1_BITS;  // bits 47..36
 constexpr int SB_SLOTS = 2 * MAX_LISTS;  // sample ranks per group (both bracket ends)
 
 // The bucket of each sample rank (block per group: block scan of the 32K bins
@@ -585,7 +586,7 @@ __global__ void __launch_bounds__(1024) sb_select0_kernel(const uint32_t* __rest
     }
 }
 
-// bits 47..33 of the sample values whose digit 0 is a selected bucket, into
+// bits 47..36 of the sample values whose digit 0 is a selected bucket, into
 // the plane of that bucket's first slot (global atomics: the values spread)
 __global__ void __launch_bounds__(256) sb_hist1_kernel(const double* __restrict__ resp, int64_t n_rows, RowView rv,
                                                        int64_t ldr, int64_t rows_per_group, int n_slots,
@@ -617,13 +618,13 @@ __global__ void __launch_bounds__(256) sb_hist1_kernel(const double* __restrict_
 #pragma unroll
                 for (int q = 0; q < SB_SLOTS; q++)
                     if (bk[q] == d0) ql = q;
-                if (ql >= 0) atomicAdd(&hg[(size_t)ql * H1_BINS + ((u[k] >> 33) & (H1_BINS - 1))], 1u);
+                if (ql >= 0) atomicAdd(&hg[(size_t)ql * H1_BINS + ((u[k] >> 36) & (H1_BINS - 1))], 1u);
             }
         }
     }
 }
 
-// per (group, slot): the bit prefix (62..33) of the sample order statistic
+// per (group, slot): the bit prefix (62..36) of the sample order statistic
 __global__ void __launch_bounds__(1024) sb_select1_kernel(const uint32_t* __restrict__ hist1, int n_slots,
                                                           const uint32_t* __restrict__ bucket,
                                                           const int64_t* __restrict__ resid,
@@ -658,7 +659,7 @@ __global__ void __launch_bounds__(1024) sb_select1_kernel(const uint32_t* __rest
             if ((int64_t)cum[mid] > r) hi = mid;
             else lo = mid + 1;
         }
-        prefix[gi] = ((uint64_t)bucket[gi] << 48) | ((uint64_t)lo << 33);
+        prefix[gi] = ((uint64_t)bucket[gi] << 48) | ((uint64_t)lo << 36);
     }
 }
 
@@ -910,7 +911,7 @@ static int select_rows(const double* d_resp, int64_t n_groups, int64_t rows_per_
     return CS_OK;
 }
 
-// Bit prefixes (62..33) of the sample order statistics at srank[g][i]
+// Bit prefixes (62..36) of the sample order statistics at srank[g][i]
 // (i < n_slots <= SB_SLOTS) over the logical view rv of every row.
 static int sample_brackets(const double* d_resp, int64_t n_groups, int64_t rows_per_group, RowView rv,
                            int64_t ldr, const std::vector<int64_t>& srank, int n_slots,
@@ -1136,7 +1137,7 @@ extern "C" int cs_rep_stats_impl(const double* d_resp, int32_t n_groups, int64_t
                 r_both[(g * 2 * n_ranks) + q] = r_lo[g * n_ranks + q];
                 r_both[(g * 2 * n_ranks) + n_ranks + q] = r_hi[g * n_ranks + q];
             }
-        std::vector<uint64_t> p_both, p_lo(T), p_hi(T);  // bit prefixes 62..33 of the sample statistics
+        std::vector<uint64_t> p_both, p_lo(T), p_hi(T);  // bit prefixes 62..36 of the sample statistics
         trace("begin", st);
         if ((rc = sample_brackets(d_resp, n_groups, rows_per_group, sample, ldr, r_both, 2 * n_ranks, p_both, dist,
                                   st)))
@@ -1156,10 +1157,10 @@ extern "C" int cs_rep_stats_impl(const double* d_resp, int32_t n_groups, int64_t
             std::vector<int> idx(n_ranks);
             for (int q = 0; q < n_ranks; q++) idx[q] = q;
             // whole high-word ranges: the row pass classifies on the high 32 bits
-            // alone (a sample statistic lies in [prefix, prefix + 2^33))
+            // alone (a sample statistic lies in [prefix, prefix + 2^36))
             auto a_of = [&](int q) { return r_lo[g * n_ranks + q] == 0 ? 0ull : p_lo[g * n_ranks + q] & ~0xffffffffull; };
             auto b_of = [&](int q) {
-                return r_hi[g * n_ranks + q] == NS - 1 ? 0x7fffffffffffffffull : p_hi[g * n_ranks + q] | 0x1ffffffffull;
+                return r_hi[g * n_ranks + q] == NS - 1 ? 0x7fffffffffffffffull : p_hi[g * n_ranks + q] | 0xfffffffffull;
             };
             std::sort(idx.begin(), idx.end(), [&](int x, int y) { return a_of(x) < a_of(y); });
             for (int q : idx) {
