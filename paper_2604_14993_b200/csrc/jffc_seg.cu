@@ -831,7 +831,22 @@ __global__ void seg_finalize_kernel(Args A) {
     double ag[NAGG];
     for (int k = 0; k < NAGG; k++) ag[k] = 0.0;
     const double* bp = A.blk + tid;
-    for (int64_t kb = 0; kb < A.nblk; kb++)
+    // the blocks in order; 8 blocks' loads issued ahead of their adds (the
+    // add chains are sequential, the loads are not)
+    constexpr int KB = 8;
+    int64_t kb = 0;
+    for (; kb + KB <= A.nblk; kb += KB) {
+        double v[KB][NAGG];
+#pragma unroll
+        for (int u = 0; u < KB; u++)
+#pragma unroll
+            for (int k = 0; k < NAGG; k++) v[u][k] = __ldcs(bp + ((kb + u) * NAGG + k) * T);
+#pragma unroll
+        for (int u = 0; u < KB; u++)
+#pragma unroll
+            for (int k = 0; k < NAGG; k++) ag[k] = __dadd_rn(ag[k], v[u][k]);
+    }
+    for (; kb < A.nblk; kb++)
         for (int k = 0; k < NAGG; k++) ag[k] = __dadd_rn(ag[k], bp[(kb * NAGG + k) * T]);
     const double w_start = pre[S], t_mid = pre[S + 1], t_end = pre[S + 2];
     cs_rep_summary out;
@@ -996,7 +1011,7 @@ static int launch(const Plan& pl, Args A, cudaStream_t st) {
             fprintf(stderr, "\n");
         }
     }
-    seg_finalize_kernel<<<(int)((pl.T + 127) / 128), 128, 0, st>>>(A);
+    seg_finalize_kernel<<<(int)((pl.T + 63) / 64), 64, 0, st>>>(A);  // >= 2 blocks per SM on config 2
     return check_launch("seg_finalize_kernel");
 }
 
