@@ -27,6 +27,8 @@
 #include <cuda_runtime.h>
 #include <math.h>
 
+#include <algorithm>
+
 #include "cs_internal.cuh"
 
 namespace cs {
@@ -183,7 +185,7 @@ struct GcaNode {
 };
 
 // true iff path(u1) ++ v  <  path(u2) ++ v  (Python tuple order on node orders)
-__device__ bool lex_less(const GcaNode* __restrict__ nd, int u1, int u2, int v) {
+__device__ __forceinline__ bool lex_less(const GcaNode* __restrict__ nd, int u1, int u2, int v) {
     if (u1 == u2) return false;
     int a = u1, b = u2;
     int da = nd[a].depth, db = nd[b].depth;
@@ -216,7 +218,21 @@ __device__ bool lex_less(const GcaNode* __restrict__ nd, int u1, int u2, int v) 
 #define GCA_SPIN_NS 20  // back-off of a warp waiting for its predecessors' buckets
 #endif
 
-__global__ void __launch_bounds__(512) gca_kernel(
+// Per-group scalars of the GCA body (a CTA, or one warp of a CTA).
+struct GcaShared {
+    int nodes, status;
+    unsigned long long edges;
+};
+
+// One placement's GCA, run by a group: the whole CTA (WARP = false: large
+// routing graphs, the warps share each round's nodes through per-bucket
+// finish counters) or one warp (WARP = true: small graphs -- a moderate-rate
+// placement uses ~90 of 1000 servers -- one instance per warp, many per CTA;
+// the warp takes the nodes in bucket order itself, no waits).  Same labels,
+// same chains either way.
+template <bool WARP>
+__device__ __forceinline__ void gca_body(
+    const int p, unsigned char* __restrict__ smem, GcaShared* __restrict__ sh,
     const cs_compose_point* __restrict__ pts, const int64_t* __restrict__ mem,
     const double* __restrict__ tau_c, const double* __restrict__ tau_p,
     const int32_t* __restrict__ id_rank, const int32_t* __restrict__ first_all,
@@ -225,7 +241,6 @@ __global__ void __launch_bounds__(512) gca_kernel(
     int32_t* __restrict__ caps_out, double* __restrict__ times_out, int32_t* __restrict__ n_chains_out,
     int64_t* __restrict__ n_edges_out, int32_t* __restrict__ status_out, int32_t max_nodes,
     int32_t max_levels) {
-    extern __shared__ unsigned char smem[];
     GcaNode* nd = reinterpret_cast<GcaNode*>(smem);
     int32_t* bucket = reinterpret_cast<int32_t*>(nd + max_nodes);  // nodes sorted by frontier
     int32_t* boff = bucket + max_nodes;                            // bucket offsets [0, L+3]
@@ -236,31 +251,31 @@ __global__ void __launch_bounds__(512) gca_kernel(
     int32_t* posn = rstamp + max_nodes;        // [max_nodes] node -> its position in `bucket`
     int32_t* pfr = posn + max_nodes;           // [max_nodes] position -> frontier of its node
     double* pcost = reinterpret_cast<double*>(((uintptr_t)(pfr + max_nodes) + 7) & ~(uintptr_t)7);  // position -> label cost
-    __shared__ int s_nodes, s_status, s_found, s_cap_fail;
-    __shared__ unsigned long long s_edges;
-    __shared__ int32_t s_path_len;
-
-    const int p = blockIdx.x;
     const cs_compose_point pt = pts[p];
     const int J = pt.n_servers;
     const int64_t sb = pt.server_base;
     const int L = (int)pt.block_count;
-    const int tid = threadIdx.x, nthr = blockDim.x;
-    const int lane = tid & 31, warp = tid >> 5, nwarps = nthr >> 5;
+    const int tid = WARP ? (int)(threadIdx.x & 31) : (int)threadIdx.x;
+    const int nthr = WARP ? 32 : (int)blockDim.x;
+    const int lane = tid & 31, warp = WARP ? 0 : tid >> 5, nwarps = nthr >> 5;
+    auto gsync = [&]() {
+        if (WARP) __syncwarp();
+        else __syncthreads();
+    };
 
     if (tid == 0) {
-        s_status = CS_OK;
-        s_edges = 0;
-        s_nodes = 0;
+        sh->status = CS_OK;
+        sh->edges = 0;
+        sh->nodes = 0;
     }
-    __syncthreads();
+    gsync();
     // --- nodes: 0 = head, then used servers (server order), last = tail ---
     if (tid == 0) {
         int v = 1;
         for (int j = 0; j < J; j++) {
             if (count_all[sb + j] <= 0) continue;
             if (v >= max_nodes - 1) {
-                s_status = CS_INVALID;
+                sh->status = CS_INVALID;
                 break;
             }
             GcaNode& n = nd[v];
@@ -273,14 +288,14 @@ __global__ void __launch_bounds__(512) gca_kernel(
             n.tp = tau_p[sb + j];
             const int64_t budget_bytes = mem[sb + j] - pt.block_bytes * (int64_t)count_all[sb + j];
             if (budget_bytes < 0) {
-                s_status = CS_INVALID;
+                sh->status = CS_INVALID;
                 break;
             }
             const int64_t budget = budget_bytes / pt.cache_slot_bytes;
             if (residual) {
                 const int64_t r = residual[sb + j];
                 if (r < 0 || r > budget) {
-                    s_status = CS_INVALID;
+                    sh->status = CS_INVALID;
                     break;
                 }
                 n.resid = r;
@@ -305,10 +320,10 @@ __global__ void __launch_bounds__(512) gca_kernel(
         t.ord = 0x7fffffff;
         t.tc = t.tp = 0.0;
         t.resid = 0;
-        s_nodes = v + 1;
+        sh->nodes = v + 1;
     }
-    __syncthreads();
-    if (s_status != CS_OK || L + 3 > max_levels) {
+    gsync();
+    if (sh->status != CS_OK || L + 3 > max_levels) {
         if (tid == 0) {
             status_out[p] = CS_INVALID;
             n_chains_out[p] = 0;
@@ -316,7 +331,7 @@ __global__ void __launch_bounds__(512) gca_kernel(
         }
         return;
     }
-    const int V = s_nodes, TAIL = V - 1;
+    const int V = sh->nodes, TAIL = V - 1;
     // --- bucket nodes by frontier (stable counting sort; V is small) ---
     if (tid == 0) {
         for (int f = 0; f <= L + 3; f++) boff[f] = 0;
@@ -336,14 +351,14 @@ __global__ void __launch_bounds__(512) gca_kernel(
         for (int f = L + 3; f > 0; f--) boff[f] = boff[f - 1];
         boff[0] = 0;
     }
-    __syncthreads();
+    gsync();
     // --- edge count (feasible_edges, model.py:179-187): sum_v |{u: a_v <= f_u <= b_v}| ---
     for (int v = 1 + tid; v < V; v += nthr) {
         const int lo = nd[v].ra, hi = nd[v].rb;
-        atomicAdd(&s_edges, (unsigned long long)(boff[hi + 1] - boff[lo]));
+        atomicAdd(&sh->edges, (unsigned long long)(boff[hi + 1] - boff[lo]));
     }
-    __syncthreads();
-    const int64_t E = (int64_t)s_edges;
+    gsync();
+    const int64_t E = (int64_t)sh->edges;
     for (int v = tid; v < V; v += nthr) {
         nd[v].cost = v == 0 ? 0.0 : INFINITY;
         nd[v].parent = -1;
@@ -356,7 +371,7 @@ __global__ void __launch_bounds__(512) gca_kernel(
         bcnt[f] = 0;
         dstamp[f] = -1;
     }
-    __syncthreads();
+    gsync();
     int K = 0;
     int64_t it = 0;
     for (it = 0; it <= E; it++) {
@@ -383,9 +398,11 @@ __global__ void __launch_bounds__(512) gca_kernel(
             bool dirty = its == 0 || rstamp[v] == its;
             for (int fb = (lo > 2 ? lo : 2); fb <= hi; fb += 32) {  // bucket 1: the head, always final
                 const int f = fb + lane;
-                const int need = f <= hi ? (its + 1) * (boff[f + 1] - boff[f]) : 0;
-                while (!__all_sync(0xffffffffu, f > hi || vcnt[f] >= need)) __nanosleep(GCA_SPIN_NS);
-                __threadfence_block();  // acquire: the predecessors' labels
+                if (!WARP) {
+                    const int need = f <= hi ? (its + 1) * (boff[f + 1] - boff[f]) : 0;
+                    while (!__all_sync(0xffffffffu, f > hi || vcnt[f] >= need)) __nanosleep(GCA_SPIN_NS);
+                    __threadfence_block();  // acquire: the predecessors' labels
+                }
                 dirty = dirty || __any_sync(0xffffffffu, f <= hi && dstamp[f] == its);
             }
             if (dirty) {
@@ -438,18 +455,18 @@ __global__ void __launch_bounds__(512) gca_kernel(
                 }
             }
             __syncwarp();
-            if (lane == 0) {
+            if (!WARP && lane == 0) {
                 __threadfence_block();  // release: the label before its count
                 atomicAdd(&bcnt[nv.fr], 1);
             }
         }
-        __syncthreads();
+        gsync();
         if (nd[TAIL].parent < 0) break;  // tail unreachable: allocation done
         // --- allocate the chain (one thread; cache_alloc.py:115-131) ---
         if (tid == 0) {
             const int len = nd[TAIL].depth - 1;  // real servers on the path
             if (K >= max_chains || len < 1 || len > max_hops) {
-                s_status = CS_INTERNAL;
+                sh->status = CS_INTERNAL;
             } else {
                 int32_t* out = chain_srv + ((int64_t)p * max_chains + K) * max_hops;
                 int v = nd[TAIL].parent;
@@ -467,7 +484,7 @@ __global__ void __launch_bounds__(512) gca_kernel(
                     u = w;
                 }
                 if (cap < 1) {
-                    s_status = CS_INTERNAL;  // "admissible hops must support at least one job"
+                    sh->status = CS_INTERNAL;  // "admissible hops must support at least one job"
                 } else {
                     PySum T;
                     T.init();
@@ -489,15 +506,72 @@ __global__ void __launch_bounds__(512) gca_kernel(
                 }
             }
         }
-        __syncthreads();
-        if (s_status != CS_OK) break;
+        gsync();
+        if (sh->status != CS_OK) break;
         K++;
     }
     if (tid == 0) {
-        if (s_status == CS_OK && it > E) s_status = CS_INTERNAL;  // no termination
-        status_out[p] = s_status;
+        if (sh->status == CS_OK && it > E) sh->status = CS_INTERNAL;  // no termination
+        status_out[p] = sh->status;
         n_chains_out[p] = K;
         n_edges_out[p] = E;
+    }
+}
+
+
+__global__ void __launch_bounds__(512, 2) gca_kernel(
+    const cs_compose_point* __restrict__ pts, const int64_t* __restrict__ mem,
+    const double* __restrict__ tau_c, const double* __restrict__ tau_p,
+    const int32_t* __restrict__ id_rank, const int32_t* __restrict__ first_all,
+    const int32_t* __restrict__ count_all, const int64_t* __restrict__ residual, int32_t max_chains,
+    int32_t max_hops, int32_t* __restrict__ chain_srv, int32_t* __restrict__ chain_len,
+    int32_t* __restrict__ caps_out, double* __restrict__ times_out, int32_t* __restrict__ n_chains_out,
+    int64_t* __restrict__ n_edges_out, int32_t* __restrict__ status_out, int32_t max_nodes,
+    int32_t max_levels) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ GcaShared sh;
+    gca_body<false>(blockIdx.x, smem, &sh, pts, mem, tau_c, tau_p, id_rank, first_all, count_all, residual,
+                    max_chains, max_hops, chain_srv, chain_len, caps_out, times_out, n_chains_out, n_edges_out,
+                    status_out, max_nodes, max_levels);
+}
+
+constexpr int GCA_GW = 8;  // instances (warps) per CTA of the warp form
+
+__global__ void __launch_bounds__(32 * GCA_GW) gca_warp_kernel(
+    int32_t n_points, size_t group_bytes, const cs_compose_point* __restrict__ pts,
+    const int64_t* __restrict__ mem, const double* __restrict__ tau_c, const double* __restrict__ tau_p,
+    const int32_t* __restrict__ id_rank, const int32_t* __restrict__ first_all,
+    const int32_t* __restrict__ count_all, const int64_t* __restrict__ residual, int32_t max_chains,
+    int32_t max_hops, int32_t* __restrict__ chain_srv, int32_t* __restrict__ chain_len,
+    int32_t* __restrict__ caps_out, double* __restrict__ times_out, int32_t* __restrict__ n_chains_out,
+    int64_t* __restrict__ n_edges_out, int32_t* __restrict__ status_out, int32_t max_nodes,
+    int32_t max_levels) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ GcaShared sh[GCA_GW];
+    const int w = threadIdx.x >> 5;
+    const int p = blockIdx.x * GCA_GW + w;
+    if (p >= n_points) return;  // whole warps: the body syncs only its own warp
+    gca_body<true>(p, smem + (size_t)w * group_bytes, &sh[w], pts, mem, tau_c, tau_p, id_rank, first_all,
+                   count_all, residual, max_chains, max_hops, chain_srv, chain_len, caps_out, times_out,
+                   n_chains_out, n_edges_out, status_out, max_nodes, max_levels);
+}
+
+// Servers a placement uses (count > 0), max over the points: the routing
+// graph's size, which picks the GCA form and sizes its shared memory.
+__global__ void __launch_bounds__(256) used_servers_kernel(const cs_compose_point* __restrict__ pts,
+                                                           const int32_t* __restrict__ count_all,
+                                                           int32_t* __restrict__ max_used) {
+    const cs_compose_point pt = pts[blockIdx.x];
+    int c = 0;
+    for (int j = threadIdx.x; j < pt.n_servers; j += blockDim.x) c += count_all[pt.server_base + j] > 0;
+    for (int d = 16; d > 0; d >>= 1) c += __shfl_down_sync(0xffffffffu, c, d);
+    __shared__ int part[8];
+    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int t = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); w++) t += part[w];
+        atomicMax(max_used, t);
     }
 }
 
@@ -542,16 +616,48 @@ extern "C" int cs_gca_batch_impl(const cs_compose_point* d_points, int32_t n_poi
                                  int32_t* d_n_chains, int64_t* d_n_edges, int32_t* d_status,
                                  void* stream) {
     if (n_points <= 0) return CS_OK;
-    const int max_nodes = max_servers + 2;
+    cudaStream_t st = (cudaStream_t)stream;
     const int max_levels = max_blocks_L + 4;
-    const size_t smem = sizeof(GcaNode) * max_nodes + sizeof(int32_t) * (max_nodes + max_levels + 1) +
-                        sizeof(int32_t) * (2 * (size_t)max_levels + 4 * (size_t)max_nodes) + sizeof(double) * max_nodes + 8;
+    auto group_bytes = [&](int nodes) {  // the body's shared-memory layout for `nodes` nodes
+        const size_t b = sizeof(GcaNode) * nodes + sizeof(int32_t) * (nodes + max_levels + 1) +
+                         sizeof(int32_t) * (2 * (size_t)max_levels + 4 * (size_t)nodes) + sizeof(double) * nodes + 8;
+        return (b + 15) & ~(size_t)15;
+    };
+    // nodes of the largest routing graph of the batch: used servers + head + tail
+    int32_t used = max_servers;
+    {
+        int32_t* d_used = nullptr;
+        if (cudaMallocAsync((void**)&d_used, sizeof(int32_t), st) == cudaSuccess) {
+            cudaMemsetAsync(d_used, 0, sizeof(int32_t), st);
+            used_servers_kernel<<<n_points, 256, 0, st>>>(d_points, d_count, d_used);
+            cudaMemcpyAsync(&used, d_used, sizeof(int32_t), cudaMemcpyDeviceToHost, st);
+            cudaFreeAsync(d_used, st);
+            if (cudaStreamSynchronize(st) != cudaSuccess) return check_launch("used_servers_kernel");
+            used = std::min(used, max_servers);
+        } else {
+            cudaGetLastError();
+        }
+    }
+    const size_t gw_bytes = group_bytes(used + 2);
+    if (gw_bytes <= 24 * 1024) {  // small graphs: one instance per warp
+        const size_t smem = gw_bytes * GCA_GW;
+        cudaFuncSetAttribute(gca_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        gca_warp_kernel<<<(n_points + GCA_GW - 1) / GCA_GW, 32 * GCA_GW, smem, st>>>(
+            n_points, gw_bytes, d_points, d_mem, d_tau_c, d_tau_p, d_id_rank, d_first, d_count, d_residual,
+            max_chains, max_hops, d_chain_srv, d_chain_len, d_caps, d_times, d_n_chains, d_n_edges, d_status,
+            used + 2, max_levels);
+        return check_launch("gca_warp_kernel");
+    }
+    // large graphs: one CTA per instance (sized by the fleet, as measured best:
+    // fewer resident CTAs keep the waiting warps from crowding the SM)
+    const int max_nodes = max_servers + 2;
+    const size_t smem = group_bytes(max_nodes);
     if (smem > 220 * 1024) {
         set_error("cs_gca_batch: %d servers per point exceeds shared memory", max_servers);
         return CS_UNSUPPORTED;
     }
     cudaFuncSetAttribute(gca_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    gca_kernel<<<n_points, 512, smem, (cudaStream_t)stream>>>(
+    gca_kernel<<<n_points, 512, smem, st>>>(
         d_points, d_mem, d_tau_c, d_tau_p, d_id_rank, d_first, d_count, d_residual, max_chains,
         max_hops, d_chain_srv, d_chain_len, d_caps, d_times, d_n_chains, d_n_edges, d_status,
         max_nodes, max_levels);
