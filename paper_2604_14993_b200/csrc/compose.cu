@@ -104,7 +104,34 @@ __global__ void __launch_bounds__(1024) gbp_kernel(
         keys[q].idx = -1;
     }
     __syncthreads();
-    // bitonic sort (ascending) of P2 keys
+    // bitonic sort (ascending) of P2 keys; one key per thread (P2 == the
+    // block): the exchanges with a partner in the same warp go through
+    // shuffles (40 of a 1024-sort's 55 steps), the others through shared memory
+    if (P2 == (int)blockDim.x) {
+        const int i = threadIdx.x;
+        SortKey my = keys[i];
+        for (int k = 2; k <= P2; k <<= 1) {
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                SortKey o;
+                if (j >= 32) {
+                    __syncthreads();
+                    keys[i] = my;
+                    __syncthreads();
+                    o = keys[i ^ j];
+                } else {
+                    o.amort = __shfl_xor_sync(0xffffffffu, my.amort, j);
+                    o.rank = __shfl_xor_sync(0xffffffffu, my.rank, j);
+                    o.idx = __shfl_xor_sync(0xffffffffu, my.idx, j);
+                }
+                const bool keep_min = ((i & k) == 0) == ((i & j) == 0);
+                const bool o_less = key_less(o, my);
+                if (keep_min == o_less) my = o;
+            }
+        }
+        __syncthreads();
+        keys[i] = my;
+        __syncthreads();
+    } else
     for (int k = 2; k <= P2; k <<= 1) {
         for (int j = k >> 1; j > 0; j >>= 1) {
             for (int i = threadIdx.x; i < P2; i += blockDim.x) {
