@@ -91,9 +91,10 @@ def run(regime: str, n_inst: int, steps: int, cpu_sample: int):
                     "is the reference-equivalent work rate; the kernel's own bound is issue/latency "
                     "(ncu issue-slot utilisation below)",
             "ncu": prof}
-    if prof and "gca_kernel" in prof and "Issue Slots Busy" in prof["gca_kernel"]:
-        roof["frac"] = float(prof["gca_kernel"]["Issue Slots Busy"].split()[-1]) / 100.0
-        roof["frac_of"] = "gca_kernel issue slots busy (ncu, profiles/r2_ncu_compose.json)"
+    gk = next((k for k in ("gca_warp_kernel", "gca_kernel") if prof and k in prof), None)
+    if gk and "Issue Slots Busy" in prof[gk]:
+        roof["frac"] = float(prof[gk]["Issue Slots Busy"].split()[-1]) / 100.0
+        roof["frac_of"] = f"{gk} issue slots busy (ncu, profiles/r2_ncu_compose.json)"
     return {
         "metric": "composed instances/sec (GBP-CR + GCA)", "regime": regime,
         "value": n_inst / (total_ms / 1e3), "unit": "instances/s", "n_gpus": 1, "steps": steps,

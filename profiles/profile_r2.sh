@@ -22,7 +22,7 @@ ncu --set full --import-source on --clock-control none -k regex:exp_streams -c 1
 for R in moderate full; do
   C="python bench_compose.py --regime $R --instances 2000 --steps 1 --cpu-sample 1"
   $C > gpurun_out/prof_compose_${R}_plain.log 2>&1 || exit 1
-  ncu --set full --import-source on --clock-control none -k regex:"gbp_kernel|gca_kernel" -c 2 \
+  ncu --set full --import-source on --clock-control none -k regex:"gbp_kernel|gca_kernel|gca_warp_kernel" -c 2 \
       -o gpurun_out/prof_compose_$R $C > gpurun_out/prof_compose_$R.log 2>&1
 done
 echo done
