@@ -13,18 +13,20 @@
 // responses (the values np.quantile interpolates between).  An exact
 // sample-select whose only full read of the responses is the leaf-sum pass:
 //   1. sample = 4 consecutive responses (one sector) of every 128 of each row
-//      (1/32 of the bytes, spread over the whole run).  Exact sample order
-//      statistics at ranks k|S|/N -+ 12 sigma bracket each target: MSB radix
-//      select on the IEEE bit patterns (responses >= +0, so bit order ==
-//      value order): 15-bit digit-0 histogram, compaction of the selected
-//      buckets, 12-bit digit rounds.
+//      (1/32 of the bytes, spread over the whole run).  The sample order
+//      statistics at ranks k|S|/N -+ 12 sigma bracket each target; they are
+//      located on the device by two histogram levels (responses >= +0, so
+//      bit order == value order): a 15-bit digit-0 histogram and a 12-bit
+//      histogram of the next bits within the selected buckets (sb_* kernels).
 //   2. the leaf-sum pass also counts the values below each bracket (whole
-//      high-word ranges: the high 32 bits decide) and compacts the values
-//      inside it (per-warp chunk reservations, no returning atomic on the
-//      append path; unused reserved slots sort above every response).
+//      high-word ranges: the high 32 bits decide) and collects the values
+//      inside it (staged per lane in shared memory by predicated stores,
+//      handed over in batches with exact reservations).
 //   3. if below <= k < below + |inside| (verified; else the bracket widens and
 //      step 2 repeats), the k-th value is found by 12-bit digit rounds over
 //      the few candidates, starting below the bracket's common bit prefix.
+//   Groups of <= 2^20 responses take an exact selection over every value
+//   (select_rows: digit-0 histogram, bucket compaction, digit rounds).
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdio.h>
@@ -159,20 +161,6 @@ __device__ __forceinline__ void cand_push(CandChunks& c, int lane, int q, int ql
     if (ql == q && slot < cap_q) dst_q[slot] = w;  // overflow: host check
 }
 
-// Seal the reservations: the current one's tail and the untouched next one.
-__device__ __forceinline__ void cand_seal(const CandChunks& c, int lane, int nl, const int64_t* __restrict__ cap_g,
-                                          const int64_t* __restrict__ off_g, double* __restrict__ cand) {
-    const double sent = __longlong_as_double(-1ll);
-    for (int q = 0; q < nl; q++) {
-        const int u = __shfl_sync(0xffffffffu, c.used, q);
-        const unsigned long long b = __shfl_sync(0xffffffffu, c.base, q);
-        const unsigned long long nb = __shfl_sync(0xffffffffu, c.next, q);
-        const unsigned long long cq = (unsigned long long)cap_g[q];
-        if (u + lane < CAND_CHUNK && b + u + lane < cq) cand[off_g[q] + b + u + lane] = sent;
-        if (nb + lane < cq) cand[off_g[q] + nb + lane] = sent;
-    }
-}
-
 // Compaction of the values whose digit 0 is one of the group's selected
 // buckets: a warp per row, chunked appends (the lists are pre-set to the
 // sentinel, so no sealing).
@@ -219,21 +207,6 @@ __global__ void __launch_bounds__(256) compact_bucket_kernel(
             }
         }
     }
-}
-
-// v[t] for a runtime t < T without local memory: a select tree over the
-// bits of t (levels of a power-of-two padding; slots >= T never chosen)
-template <int T>
-__device__ __forceinline__ double pick_slot(const double (&v)[T], int t) {
-    double l1[8], l2[4], l3[2];
-#pragma unroll
-    for (int i = 0; i < 8; i++)
-        l1[i] = (t & 1) ? v[2 * i + 1 < T ? 2 * i + 1 : T - 1] : v[2 * i < T ? 2 * i : T - 1];
-#pragma unroll
-    for (int i = 0; i < 4; i++) l2[i] = (t & 2) ? l1[2 * i + 1] : l1[2 * i];
-#pragma unroll
-    for (int i = 0; i < 2; i++) l3[i] = (t & 4) ? l2[2 * i + 1] : l2[2 * i];
-    return (t & 8) ? l3[1] : l3[0];
 }
 
 // bit if d[q] <= wid[q] for some q, else 0: one predicate chained through
@@ -757,12 +730,6 @@ struct DBuf {
         return (T*)p;
     }
 };
-
-static uint64_t bits_of(double d) {
-    uint64_t u;
-    memcpy(&u, &d, 8);
-    return u;
-}
 
 // 12-bit digit rounds at shifts first_shift, first_shift-12, ..., 0 (first_shift
 // a multiple of 12); slot prefixes must already hold the bits above first_shift+12.
