@@ -284,7 +284,8 @@ __global__ void __launch_bounds__(LB_WARPS * 32, 2) row_stats_kernel(
     const uint64_t* __restrict__ lo, const uint64_t* __restrict__ hi, const int64_t* __restrict__ off,
     const int64_t* __restrict__ cap, unsigned long long* __restrict__ fill,
     unsigned long long* __restrict__ below, unsigned long long* __restrict__ inside,
-    double* __restrict__ cand, int32_t n_heights, double* __restrict__ leaf_scratch, int32_t stg_slots) {
+    double* __restrict__ cand, int32_t n_heights, double* __restrict__ leaf_scratch, int32_t stg_slots,
+    int32_t plan_in_smem) {
     // shared: per-warp leaf values [LB_WARPS][L] doubles, then the plan:
     // leaf offset[L], leaf length[L], height offsets[n_heights + 1] and the
     // internal nodes in height order as (a, b) pairs: v[a] = v[a] + v[b]
@@ -294,9 +295,13 @@ __global__ void __launch_bounds__(LB_WARPS * 32, 2) row_stats_kernel(
     const int STG = stg_slots;  // >= T + 3
     double* stage_sh = row_sh;  // [LB_WARPS][STG][32]
     double* leaf_sh = row_sh + (size_t)LB_WARPS * STG * 32;
-    int32_t* plan = reinterpret_cast<int32_t*>(leaf_scratch ? leaf_sh : leaf_sh + (size_t)LB_WARPS * L);
+    // the plan: in shared memory, or (long rows: 4 words per leaf) read
+    // through L1 from global memory, which keeps two blocks per SM
+    int32_t* plan_sh = reinterpret_cast<int32_t*>(leaf_scratch ? leaf_sh : leaf_sh + (size_t)LB_WARPS * L);
     const int plan_words = 2 * L + (n_heights + 1) + 2 * (L - 1);
-    for (int q = threadIdx.x; q < plan_words; q += blockDim.x) plan[q] = g_plan[q];
+    if (plan_in_smem)
+        for (int q = threadIdx.x; q < plan_words; q += blockDim.x) plan_sh[q] = g_plan[q];
+    const int32_t* plan = plan_in_smem ? plan_sh : g_plan;
     __syncthreads();
     const int32_t* leaf_off = plan;
     const int32_t* leaf_len = plan + L;
@@ -1023,10 +1028,12 @@ extern "C" int cs_rep_stats_impl(const double* d_resp, int32_t n_groups, int64_t
     // warp, L2-resident), the plan
     auto stage_bytes = [&](int stg) { return sizeof(double) * LB_WARPS * 32 * (size_t)stg; };
     const size_t lv_bytes = sizeof(double) * LB_WARPS * (size_t)L;
-    const bool leaves_in_smem = stage_bytes(t_slots + 28) + lv_bytes + plan_bytes <= 110 * 1024;
+    const bool plan_in_smem = plan_bytes <= 32 * 1024;  // long rows (config 5: 160 KB): global, L1-cached
+    const size_t plan_sm = plan_in_smem ? plan_bytes : 0;
+    const bool leaves_in_smem = stage_bytes(t_slots + 28) + lv_bytes + plan_sm <= 110 * 1024;
     int stg = t_slots + 28;
-    while (stg > t_slots + 3 && stage_bytes(stg) + (leaves_in_smem ? lv_bytes : 0) + plan_bytes > 224 * 1024) stg--;
-    const size_t smem = stage_bytes(stg) + (leaves_in_smem ? lv_bytes : 0) + plan_bytes;
+    while (stg > t_slots + 3 && stage_bytes(stg) + (leaves_in_smem ? lv_bytes : 0) + plan_sm > 224 * 1024) stg--;
+    const size_t smem = stage_bytes(stg) + (leaves_in_smem ? lv_bytes : 0) + plan_sm;
     if (smem > 224 * 1024) {
         set_error("cs_rep_stats: rows of %lld responses exceed the on-chip pairwise plan", (long long)m);
         return CS_UNSUPPORTED;
@@ -1064,7 +1071,7 @@ extern "C" int cs_rep_stats_impl(const double* d_resp, int32_t n_groups, int64_t
                                    : (slots12 ? row_stats_kernel<MAX_LISTS, 12> : row_stats_kernel<MAX_LISTS, 16>);
         k<<<blocks, LB_WARPS * 32, std::max<size_t>(smem, 16), st>>>(
             d_resp, n_rows, rows_per_group, ldr, m, b_plan.as<int32_t>(), L, d_summ, d_row_sums, do_bracket,
-            nl, lo, hi, off, cap, fill, below, inside, cand, n_heights, leaf_scratch, stg);
+            nl, lo, hi, off, cap, fill, below, inside, cand, n_heights, leaf_scratch, stg, plan_in_smem ? 1 : 0);
         return check_launch("row_stats_kernel");
     };
     const RowView full{m, 40, 40};  // contiguous
