@@ -646,6 +646,8 @@ struct SelSlot {
     int64_t rank;      // remaining rank among the candidates sharing the prefix
     int64_t cand_off;  // candidate list
     int64_t cand_len;
+    int32_t shift0;    // this slot's first digit (its candidates share every bit above it)
+    int32_t pad;
 };
 
 // Histogram of the digit [shift, shift+12) over each slot's candidates that
@@ -656,6 +658,7 @@ __global__ void __launch_bounds__(512) round_hist_kernel(const double* __restric
     __shared__ uint32_t sh[RD_BINS];
     const int s = blockIdx.y;
     const SelSlot sl = slots[s];
+    if (shift > sl.shift0) return;  // the digit is part of the slot's common prefix
     for (int b = threadIdx.x; b < RD_BINS; b += blockDim.x) sh[b] = 0;
     __syncthreads();
     const uint64_t hi_mask = shift + RD_BITS >= 64 ? 0ull : ~((1ull << (shift + RD_BITS)) - 1);
@@ -673,6 +676,7 @@ __global__ void __launch_bounds__(512) round_hist_kernel(const double* __restric
 __global__ void __launch_bounds__(1024) round_select_kernel(SelSlot* __restrict__ slots, int shift,
                                                             const uint32_t* __restrict__ hist) {
     const int s = blockIdx.x;
+    if (shift > slots[s].shift0) return;
     __shared__ unsigned long long part[1024];
     const uint32_t* h = hist + (int64_t)s * RD_BINS;
     constexpr int PER = RD_BINS / 1024;
@@ -852,6 +856,7 @@ static int select_rows(const double* d_resp, int64_t n_groups, int64_t rows_per_
             }
             SelSlot& s = slots[g * n_ranks + q];
             s.prefix = (uint64_t)b << 48;
+            s.shift0 = 36;  // bits 47..0 below the digit-0 bucket
             s.rank = rank - c;
             s.cand_off = off[g * SEL_LISTS + list];
             s.cand_len = cap[g * SEL_LISTS + list];
@@ -1224,7 +1229,13 @@ extern "C" int cs_rep_stats_impl(const double* d_resp, int32_t n_groups, int64_t
                 ok = false;
                 break;
             }
-            slots[i].prefix = lo[li] & keep;  // bits shared by every candidate of the bracket
+            // the slot's own first digit: below its bracket's highest differing bit
+            const uint64_t dlh = lo[li] ^ hi[li];
+            const int tb = dlh ? 63 - __builtin_clzll(dlh) : 0;
+            const int sh0 = std::min(first_shift, (tb / RD_BITS) * RD_BITS);
+            const uint64_t keep_s = sh0 + RD_BITS >= 64 ? 0ull : ~((1ull << (sh0 + RD_BITS)) - 1);
+            slots[i].shift0 = sh0;
+            slots[i].prefix = lo[li] & keep_s;  // bits shared by every candidate of the bracket
             slots[i].rank = k - (int64_t)below[li];
             slots[i].cand_off = off[li];
             slots[i].cand_len = (int64_t)fill[li];  // this rank's candidates
