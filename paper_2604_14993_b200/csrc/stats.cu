@@ -1196,6 +1196,10 @@ extern "C" int cs_rep_stats_impl(const double* d_resp, int32_t n_groups, int64_t
         // included); inside = values actually inside the brackets
         std::vector<unsigned long long> fill(L6), below(L6), inside_all(L6), overflow(L6);
         cudaMemcpyAsync(fill.data(), b_fill.p, b_fill.n, cudaMemcpyDeviceToHost, st);
+        if (!dist) {  // one read-back of all the counts
+            cudaMemcpyAsync(inside_all.data(), b_inside.p, b_inside.n, cudaMemcpyDeviceToHost, st);
+            cudaMemcpyAsync(below.data(), b_below.p, b_below.n, cudaMemcpyDeviceToHost, st);
+        }
         if ((rc = check_cuda(cudaStreamSynchronize(st), "bracket sync"))) return rc;
         for (size_t li = 0; li < L6; li++) overflow[li] = (int64_t)fill[li] > cap[li] ? 1 : 0;
         if (dist) {  // global below / inside counts and any-rank overflow
@@ -1206,10 +1210,10 @@ extern "C" int cs_rep_stats_impl(const double* d_resp, int32_t n_groups, int64_t
                 (rc = allreduce_max_u64(b_ov.p, L6, st)))
                 return rc;
             cudaMemcpyAsync(overflow.data(), b_ov.p, 8 * L6, cudaMemcpyDeviceToHost, st);
+            cudaMemcpyAsync(inside_all.data(), b_inside.p, b_inside.n, cudaMemcpyDeviceToHost, st);
+            cudaMemcpyAsync(below.data(), b_below.p, b_below.n, cudaMemcpyDeviceToHost, st);
+            if ((rc = check_cuda(cudaStreamSynchronize(st), "bracket sync 2"))) return rc;
         }
-        cudaMemcpyAsync(inside_all.data(), b_inside.p, b_inside.n, cudaMemcpyDeviceToHost, st);
-        cudaMemcpyAsync(below.data(), b_below.p, b_below.n, cudaMemcpyDeviceToHost, st);
-        if ((rc = check_cuda(cudaStreamSynchronize(st), "bracket sync 2"))) return rc;
         trace("row pass+counts", st);
         // ---- 3. verify the brackets, exact rounds over the candidates ----
         const int first_shift = (top_bit / RD_BITS) * RD_BITS;  // digits cover bits <= top_bit
