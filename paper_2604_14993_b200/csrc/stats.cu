@@ -647,24 +647,26 @@ struct SelSlot {
     int64_t cand_off;  // candidate list
     int64_t cand_len;
     int32_t shift0;    // this slot's first digit (its candidates share every bit above it)
-    int32_t pad;
+    int32_t compacted; // 1: cand_off/cand_len index the compacted candidates
 };
 
 // Histogram of the digit [shift, shift+12) over each slot's candidates that
 // match its prefix; shared-memory privatised (candidates cluster in few bins).
 __global__ void __launch_bounds__(512) round_hist_kernel(const double* __restrict__ cand,
+                                                         const double* __restrict__ ccand,
                                                          const SelSlot* __restrict__ slots, int n_slots,
                                                          int shift, uint32_t* __restrict__ hist) {
     __shared__ uint32_t sh[RD_BINS];
     const int s = blockIdx.y;
     const SelSlot sl = slots[s];
     if (shift > sl.shift0) return;  // the digit is part of the slot's common prefix
+    const double* __restrict__ src = sl.compacted ? ccand : cand;
     for (int b = threadIdx.x; b < RD_BINS; b += blockDim.x) sh[b] = 0;
     __syncthreads();
     const uint64_t hi_mask = shift + RD_BITS >= 64 ? 0ull : ~((1ull << (shift + RD_BITS)) - 1);
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < sl.cand_len;
          i += (int64_t)gridDim.x * blockDim.x) {
-        const uint64_t u = dbits(cand[sl.cand_off + i]);
+        const uint64_t u = dbits(src[sl.cand_off + i]);
         if ((u & hi_mask) == sl.prefix) atomicAdd(&sh[(u >> shift) & (RD_BINS - 1)], 1u);
     }
     __syncthreads();
@@ -742,6 +744,42 @@ struct DBuf {
 
 // 12-bit digit rounds at shifts first_shift, first_shift-12, ..., 0 (first_shift
 // a multiple of 12); slot prefixes must already hold the bits above first_shift+12.
+// After every slot's first digit round the candidates still sharing its
+// prefix are few: copy them out (per slot, into its own region) so the later
+// rounds read only those.  A slot whose matches overflow its region keeps
+// its list.
+__global__ void __launch_bounds__(512) round_compact_kernel(const double* __restrict__ cand,
+                                                            const SelSlot* __restrict__ slots, int shift,
+                                                            double* __restrict__ out, int64_t region,
+                                                            unsigned long long* __restrict__ cnt) {
+    const int s = blockIdx.y, lane = threadIdx.x & 31;
+    const SelSlot sl = slots[s];
+    const uint64_t hi_mask = shift >= 64 ? 0ull : ~((1ull << shift) - 1);
+    double* dst = out + (int64_t)s * region;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); i0 < sl.cand_len; i0 += stride) {
+        const int64_t i = i0 + lane;
+        const double v = i < sl.cand_len ? cand[sl.cand_off + i] : 0.0;
+        const bool m = i < sl.cand_len && (dbits(v) & hi_mask) == sl.prefix;
+        const unsigned bal = __ballot_sync(0xffffffffu, m);
+        if (!bal) continue;
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(&cnt[s], (unsigned long long)__popc(bal));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        const unsigned long long pos = base + __popc(bal & ((1u << lane) - 1u));
+        if (m && pos < (unsigned long long)region) dst[pos] = v;
+    }
+}
+
+__global__ void round_compact_fix_kernel(SelSlot* __restrict__ slots, int n_slots, int64_t region,
+                                         const unsigned long long* __restrict__ cnt) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n_slots || cnt[s] > (unsigned long long)region) return;
+    slots[s].cand_off = (int64_t)s * region;
+    slots[s].cand_len = (int64_t)cnt[s];
+    slots[s].compacted = 1;
+}
+
 static int run_rounds(std::vector<SelSlot>& slots, const double* d_cand, int first_shift, bool dist,
                       cudaStream_t st) {
     const int n_slots = (int)slots.size();
@@ -755,14 +793,33 @@ static int run_rounds(std::vector<SelSlot>& slots, const double* d_cand, int fir
     int64_t max_len = 1;
     for (auto& s : slots) max_len = std::max(max_len, s.cand_len);
     const int bx = (int)std::max<int64_t>(1, std::min<int64_t>((max_len + 4095) / 4096, 64));
+    // after the round at the lowest first digit every slot has had its first
+    // round: compact there if more rounds follow
+    int min_shift0 = first_shift;
+    for (auto& s : slots) min_shift0 = std::min(min_shift0, (int)s.shift0);
+    const int64_t region = std::max<int64_t>(4096, max_len / 32);
+    DBuf b_ccand, b_ccnt;
     for (int shift = first_shift; shift >= 0; shift -= RD_BITS) {
         cudaMemsetAsync(b_hist.p, 0, b_hist.n, st);
-        round_hist_kernel<<<dim3(bx, n_slots), 512, 0, st>>>(d_cand, b_slots.as<SelSlot>(), n_slots, shift,
-                                                              b_hist.as<uint32_t>());
+        round_hist_kernel<<<dim3(bx, n_slots), 512, 0, st>>>(d_cand, b_ccand.as<double>(), b_slots.as<SelSlot>(),
+                                                              n_slots, shift, b_hist.as<uint32_t>());
         if ((rc = check_launch("round_hist_kernel"))) return rc;
         if (dist && (rc = allreduce_u32(b_hist.p, (size_t)RD_BINS * n_slots, st))) return rc;
         round_select_kernel<<<n_slots, 1024, 0, st>>>(b_slots.as<SelSlot>(), shift, b_hist.as<uint32_t>());
         if ((rc = check_launch("round_select_kernel"))) return rc;
+        if (shift == min_shift0 && shift > 0 && max_len > 4 * region) {
+            if ((rc = b_ccand.alloc(sizeof(double) * region * (size_t)n_slots, st)) ||
+                (rc = b_ccnt.alloc(sizeof(unsigned long long) * n_slots, st)))
+                return rc;
+            cudaMemsetAsync(b_ccnt.p, 0, b_ccnt.n, st);
+            round_compact_kernel<<<dim3(bx, n_slots), 512, 0, st>>>(d_cand, b_slots.as<SelSlot>(), shift,
+                                                                     b_ccand.as<double>(), region,
+                                                                     b_ccnt.as<unsigned long long>());
+            if ((rc = check_launch("round_compact_kernel"))) return rc;
+            round_compact_fix_kernel<<<(n_slots + 127) / 128, 128, 0, st>>>(b_slots.as<SelSlot>(), n_slots, region,
+                                                                             b_ccnt.as<unsigned long long>());
+            if ((rc = check_launch("round_compact_fix_kernel"))) return rc;
+        }
     }
     cudaMemcpyAsync(slots.data(), b_slots.p, b_slots.n, cudaMemcpyDeviceToHost, st);
     return check_cuda(cudaStreamSynchronize(st), "rounds sync");
