@@ -473,6 +473,11 @@ def main():
         sim_inst = sum(k[x]["inst_executed"] for x in sim_k)
         roof["achieved"] = sim_inst / (sim_ms / 1e3)
         roof["frac"] = roof["achieved"] / issue_peak
+        # the simulator runs as whole-SM blocks of 16 warps on ceil(units/16)
+        # SMs (the others hold the next sweep's streams): its own issue share
+        occ = min(sms, -(-plan["segments"] * plan["warps_per_segment"] // 16))
+        roof["occupied_sms"] = occ
+        roof["frac_of_occupied_sms"] = roof["achieved"] / (occ * 4 * sm_hz)
         roof["traffic"] = sum(k[x]["dram_read"] + k[x]["dram_write"] for x in sim_k)
         roof["ncu"] = {"source": os.path.relpath(NCU_SUMMARY, ROOT), "inst_executed_per_sweep": sim_inst,
                        "kernels": {x: k[x] for x in sim_k}}
