@@ -1259,16 +1259,17 @@ extern "C" int cs_rep_stats_impl(const double* d_resp, int32_t n_groups, int64_t
         }
         if ((rc = check_cuda(cudaStreamSynchronize(st), "bracket sync"))) return rc;
         for (size_t li = 0; li < L6; li++) overflow[li] = (int64_t)fill[li] > cap[li] ? 1 : 0;
-        if (dist) {  // global below / inside counts and any-rank overflow
-            DBuf b_ov;
-            if ((rc = b_ov.alloc(8 * L6, st))) return rc;
-            cudaMemcpyAsync(b_ov.p, overflow.data(), 8 * L6, cudaMemcpyHostToDevice, st);
-            if ((rc = allreduce_u64(b_below.p, L6, st)) || (rc = allreduce_u64(b_inside.p, L6, st)) ||
-                (rc = allreduce_max_u64(b_ov.p, L6, st)))
-                return rc;
-            cudaMemcpyAsync(overflow.data(), b_ov.p, 8 * L6, cudaMemcpyDeviceToHost, st);
-            cudaMemcpyAsync(inside_all.data(), b_inside.p, b_inside.n, cudaMemcpyDeviceToHost, st);
-            cudaMemcpyAsync(below.data(), b_below.p, b_below.n, cudaMemcpyDeviceToHost, st);
+        if (dist) {  // global below / inside counts and any-rank overflow: one all-reduce (sum)
+            DBuf b_cnt3;
+            if ((rc = b_cnt3.alloc(3 * 8 * L6, st))) return rc;
+            char* c3 = (char*)b_cnt3.p;
+            cudaMemcpyAsync(c3, b_below.p, 8 * L6, cudaMemcpyDeviceToDevice, st);
+            cudaMemcpyAsync(c3 + 8 * L6, b_inside.p, 8 * L6, cudaMemcpyDeviceToDevice, st);
+            cudaMemcpyAsync(c3 + 16 * L6, overflow.data(), 8 * L6, cudaMemcpyHostToDevice, st);
+            if ((rc = allreduce_u64(c3, 3 * L6, st))) return rc;
+            cudaMemcpyAsync(below.data(), c3, 8 * L6, cudaMemcpyDeviceToHost, st);
+            cudaMemcpyAsync(inside_all.data(), c3 + 8 * L6, 8 * L6, cudaMemcpyDeviceToHost, st);
+            cudaMemcpyAsync(overflow.data(), c3 + 16 * L6, 8 * L6, cudaMemcpyDeviceToHost, st);  // > 0: some rank
             if ((rc = check_cuda(cudaStreamSynchronize(st), "bracket sync 2"))) return rc;
         }
         trace("row pass+counts", st);
